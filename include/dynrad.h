@@ -1,0 +1,220 @@
+/* dynrad.h — C ABI of the B200-native DynamicRad sparse-attention hot path.
+ *
+ * This is the drop-in boundary.  The reference (arxiv/paper_2604_20470,
+ * `radialplan`) exposes the path as a C++ library API in namespace
+ * radialplan (proj/include/radialplan/*.hpp); it has no extern "C" layer.
+ * Each entry point below names the reference interface it replaces.  The C++
+ * facade in include/radialplan_b200/radialplan.hpp re-exposes the reference
+ * signatures on top of these calls, and INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Device buffers are caller-allocated and stream-ordered; every call that
+ *    takes a cudaStream_t only enqueues work unless documented otherwise.
+ *  - Errors: an rp_status whose codes map 1:1 onto the reference's exception
+ *    types, with the reference's message text available from
+ *    rp_last_error() (thread-local).  There is no CPU fallback: without a
+ *    CUDA device every compute entry point returns RP_CUDA_ERROR.
+ *  - Bit-packed block masks use the reference layout (mask.hpp:13-35):
+ *    row-major, LSB-first, row_bytes = ceil(S_b / 8).
+ */
+#ifndef DYNRAD_H
+#define DYNRAD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* rp_stream; /* == cudaStream_t */
+
+typedef enum {
+  RP_OK = 0,
+  RP_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  RP_OUT_OF_RANGE = 2,     /* std::out_of_range */
+  RP_DOMAIN_ERROR = 3,     /* std::domain_error */
+  RP_RUNTIME_ERROR = 4,    /* std::runtime_error */
+  RP_CUDA_ERROR = 5        /* CUDA failure / no device (no CPU fallback) */
+} rp_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* rp_last_error(void);
+/* Library version string. */
+const char* rp_version(void);
+
+/* ------------------------------------------------------------------ grid --
+ * radialplan::GridSpec / make_grid (grid.hpp:13-42). */
+typedef struct {
+  int n_frames;
+  int tokens_per_frame;
+  int block_size;
+  int64_t total_tokens;   /* S  = n_frames * tokens_per_frame */
+  int64_t padded_tokens;  /* S' = ceil(S / B) * B */
+  int64_t blocks_per_dim; /* S_b = S' / B */
+  int64_t row_bytes;      /* ceil(S_b / 8) */
+} rp_grid;
+
+rp_status rp_make_grid(int n_frames, int tokens_per_frame, int block_size,
+                       rp_grid* out);
+
+/* --------------------------------------------------------------- config --
+ * radialplan::SparsityConfig + RadialParams (selection.hpp:19-29,
+ * radial.hpp:16-20); defaults as in the reference. */
+typedef enum { RP_STATIC_RATIO = 0, RP_DYNAMIC_THRESHOLD = 1 } rp_mode;
+
+typedef struct {
+  int mode;                 /* rp_mode */
+  double decay_factor;      /* gamma */
+  double long_range_factor; /* lambda */
+  double split_epsilon;
+  double mask_threshold; /* theta_m */
+  double col_threshold;  /* theta_c */
+  double near_param;     /* rho1 or tau1 */
+  double far_param;      /* rho2 or tau2 */
+  int fallback_k;
+} rp_config;
+
+void rp_config_defaults(rp_config* c);
+/* SparsityConfig::validate (selection.cpp:11-32). */
+rp_status rp_config_validate(const rp_config* c);
+
+/* Per ordered frame pair scalars: window_width, frame_retained, pair_count,
+ * distance_tier, split_factor (radial.cpp:30-121, selection.cpp:34-59). */
+typedef struct {
+  int64_t width;
+  int retained;
+  int64_t pair_count;
+  int tier;
+  int64_t split_factor;
+  double retention_or_threshold; /* retention_ratio or score_threshold */
+} rp_frame_pair;
+rp_status rp_frame_pair_info(const rp_grid* g, const rp_config* c, int frame_i,
+                             int frame_j, rp_frame_pair* out);
+
+/* ---------------------------------------------------------------- tensors --
+ * A [tokens, heads, head_dim] view; strides in elements.  The reference's
+ * FeatureBatch holds one column-major matrix per head (attention.hpp:18-27);
+ * the facade packs those into this layout. */
+typedef enum { RP_F32 = 0, RP_BF16 = 1 } rp_dtype;
+
+typedef struct {
+  void* data; /* device pointer */
+  int dtype;  /* rp_dtype */
+  int64_t tokens;
+  int heads;
+  int head_dim;
+  int64_t token_stride; /* elements between consecutive tokens */
+  int64_t head_stride;  /* elements between consecutive heads */
+} rp_tensor;
+
+/* ------------------------------------------------------------ mask build --
+ * radialplan::build_mask (mask.hpp:88-89, mask.cpp:162-289): stages (a)
+ * candidates, (b) proxy scoring, (c) selection + theta_c/theta_m block
+ * aggregation, OR-merged into a bit-packed S_b x S_b mask.
+ *
+ * A plan caches everything that depends only on (grid, config, seed,
+ * options): the frame-pair job table, the content-independent base mask
+ * (intra-frame rectangles + full bands), and in static mode the whole mask.
+ * Static masks are built once (first call) and re-emitted from the cache,
+ * matching the paper's precomputed static masks. */
+typedef struct rp_plan_s* rp_plan;
+
+typedef struct {
+  int disable_split; /* BuildOptions::disable_split (mask.hpp:77-81) */
+  /* Dynamic mode scoring engine: 0 = auto, 1 = tensor-core scores with an
+   * exact fp64 recheck of every pair within `recheck_delta` of its
+   * threshold, 2 = exact fp64 SIMT scores + sequential per-pair statistics
+   * (bit-identical to the reference; for small grids and fp32 features). */
+  int score_engine;
+  double recheck_delta; /* in z units; <= 0 selects the default (1e-4) */
+} rp_build_options;
+
+typedef struct {
+  int64_t retained_frame_pairs; /* BuildTimings::retained_frame_pairs */
+  int64_t scored_pairs;         /* BuildTimings::scored_pairs */
+  int64_t sampled_pairs;        /* static: Fisher-Yates draws */
+  int64_t rechecked_pairs;      /* dynamic fast engine: fp64 rechecks */
+  int64_t fallback_frame_pairs; /* dynamic: pairs that used fallback_k */
+  int64_t active_blocks;        /* popcount of the mask */
+} rp_build_stats;
+
+void rp_build_options_defaults(rp_build_options* o);
+rp_status rp_plan_create(const rp_grid* g, const rp_config* c, uint64_t seed,
+                         const rp_build_options* opt, rp_plan* out);
+void rp_plan_destroy(rp_plan p);
+
+/* Build the mask for one layer into mask_bits_dev (S_b * row_bytes bytes,
+ * device).  q/k: the scoring features (the first n_score_heads heads of the
+ * layer's Q/K are used, H_f in the paper; FeatureBatch::heads in the
+ * reference); required in dynamic mode, ignored (may be NULL) in static
+ * mode.  stats may be NULL; filling it synchronizes the stream. */
+rp_status rp_plan_build_mask(rp_plan p, const rp_tensor* q, const rp_tensor* k,
+                             int n_score_heads, uint8_t* mask_bits_dev,
+                             rp_build_stats* stats, rp_stream stream);
+
+/* One-shot convenience: plan + build + destroy, synchronous. */
+rp_status rp_build_mask(const rp_grid* g, const rp_config* c, uint64_t seed,
+                        const rp_build_options* opt, const rp_tensor* q,
+                        const rp_tensor* k, int n_score_heads,
+                        uint8_t* mask_bits_dev, rp_build_stats* stats,
+                        rp_stream stream);
+
+/* -------------------------------------------------------- mask utilities --
+ * Block-sparse row lists (new; the reference stops at the bitmask):
+ * row_ptr[S_b+1], col_idx[col_cap] (ascending per row), row_order[S_b]
+ * (rows by descending nnz, ties by index; may be NULL), nnz_dev[1] (may be
+ * NULL).  Fails with RP_OUT_OF_RANGE (reported asynchronously through
+ * nnz > col_cap) if the mask has more active blocks than col_cap. */
+rp_status rp_mask_to_csr(const rp_grid* g, const uint8_t* mask_bits_dev,
+                         int32_t* row_ptr_dev, int32_t* col_idx_dev,
+                         int64_t col_cap, int32_t* row_order_dev,
+                         int64_t* nnz_dev, rp_stream stream);
+
+/* expand_mask (mask.cpp:52-66): token-level bits, S' x ceil(S'/8) bytes. */
+rp_status rp_expand_mask(const rp_grid* g, const uint8_t* mask_bits_dev,
+                         uint8_t* token_bits_dev, rp_stream stream);
+
+/* sparsity (mask.cpp:47-50) and active-block count; synchronous. */
+rp_status rp_mask_sparsity(const rp_grid* g, const uint8_t* mask_bits_dev,
+                           int64_t* active_blocks, double* sparsity,
+                           rp_stream stream);
+
+/* ------------------------------------------------------ sparse attention --
+ * masked_attention_exact (attention.hpp:43-44, attention.cpp:50-121): per
+ * head, O = softmax(Q K^T * scale restricted to active blocks) V over the
+ * padded token axis.  Padding rows of Q/K/V (tokens >= S) are zeros and
+ * take part as keys whenever their block is active (attention.cpp:43-48).
+ * o: [S', heads, head_dim], same dtype as q.
+ *   bf16: tcgen05/TMEM/TMA block-sparse flash forward (requires B = 128 and
+ *         head_dim in {64, 128}); fp32 softmax.
+ *   f32 : exact-precision path (fp32 logits, fp64 softmax), any B.
+ * softmax_scale <= 0 selects 1/sqrt(head_dim).  row_order may be NULL. */
+rp_status rp_sparse_attention_fwd(const rp_grid* g, const rp_tensor* q,
+                                  const rp_tensor* k, const rp_tensor* v,
+                                  rp_tensor* o, const int32_t* row_ptr_dev,
+                                  const int32_t* col_idx_dev,
+                                  const int32_t* row_order_dev,
+                                  float softmax_scale, rp_stream stream);
+
+/* Host-buffer convenience with the reference's calling convention: host
+ * Q/K/V [tokens, heads, d] (pinned or pageable; dtype f32 or bf16), host
+ * bit-packed block mask; host output [S', heads, d].  Copies in, builds the
+ * row lists, runs the kernel, copies out, synchronizes.  Throws
+ * RP_DOMAIN_ERROR when a row has no active block (attention.cpp:85-86). */
+rp_status rp_masked_attention_exact_host(const rp_grid* g,
+                                         const uint8_t* mask_bits_host,
+                                         const void* q_host, const void* k_host,
+                                         const void* v_host, int dtype,
+                                         int64_t tokens, int heads,
+                                         int head_dim, void* o_host,
+                                         rp_stream stream);
+
+/* Number of CUDA kernels this library has launched in the calling process
+ * (all entry points); used by bench.py to report gpu_launches. */
+int64_t rp_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNRAD_H */

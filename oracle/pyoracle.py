@@ -1,0 +1,324 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the two CPU checkers.
+
+* ``ref``  : oracle/_ref/libradialplan_ref.so, the reference's own
+             radialplan sources compiled in place (oracle/Makefile).
+* ``port`` : oracle/liboracle.so, our plain-C restatement
+             (oracle/radialplan_oracle.c).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline legs may
+import this module.  The product path (paper_2604_20470_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libradialplan_ref.so")
+PORT_SO = os.path.join(HERE, "liboracle.so")
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class _Cfg(C.Structure):
+    _fields_ = [
+        ("mode", C.c_int),
+        ("decay_factor", C.c_double),
+        ("long_range_factor", C.c_double),
+        ("split_epsilon", C.c_double),
+        ("mask_threshold", C.c_double),
+        ("col_threshold", C.c_double),
+        ("near_param", C.c_double),
+        ("far_param", C.c_double),
+        ("fallback_k", C.c_int),
+    ]
+
+
+class _Grid(C.Structure):
+    _fields_ = [
+        ("n_frames", C.c_int),
+        ("tokens_per_frame", C.c_int),
+        ("block_size", C.c_int),
+        ("total_tokens", C.c_int64),
+        ("padded_tokens", C.c_int64),
+        ("blocks_per_dim", C.c_int64),
+        ("row_bytes", C.c_int64),
+    ]
+
+
+@dataclass
+class Cfg:
+    """Mirror of radialplan::SparsityConfig (selection.hpp:19-29)."""
+
+    mode: int = 0  # 0 static ratio, 1 dynamic threshold
+    decay_factor: float = 1.0
+    long_range_factor: float = 1.0
+    split_epsilon: float = 1e-6
+    mask_threshold: float = 0.75
+    col_threshold: float = 0.20
+    near_param: float = 0.25
+    far_param: float = 0.55
+    fallback_k: int = 1
+
+    def c(self):
+        return _Cfg(self.mode, self.decay_factor, self.long_range_factor,
+                    self.split_epsilon, self.mask_threshold, self.col_threshold,
+                    self.near_param, self.far_param, self.fallback_k)
+
+
+def grid_dims(nf, nt, bs):
+    total = nf * nt
+    padded = (total + bs - 1) // bs * bs
+    blocks = padded // bs
+    return total, padded, blocks, (blocks + 7) // 8
+
+
+_P = C.POINTER
+_f32p = _P(C.c_float)
+_u8p = _P(C.c_uint8)
+
+
+def _fp(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_f32p)
+
+
+class _Lib:
+    def __init__(self, path, kind):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        self.kind = kind
+        self.lib = C.CDLL(path)
+
+
+_ref = None
+_port = None
+
+
+def have_ref():
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        _ref = _RefLib(REF_SO, "reference")
+    return _ref
+
+
+def port():
+    global _port
+    if _port is None:
+        _port = _PortLib(PORT_SO, "port")
+    return _port
+
+
+def _feat(q, k):
+    if q is None:
+        return None, None, 0, 0, 0
+    assert q.shape == k.shape and q.ndim == 3
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    k = np.ascontiguousarray(k, dtype=np.float32)
+    return q, k, q.shape[0], q.shape[1], q.shape[2]
+
+
+class _RefLib(_Lib):
+    def __init__(self, path, kind):
+        super().__init__(path, kind)
+        L = self.lib
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_build_mask.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_uint64, C.c_int,
+                                     _f32p, _f32p, C.c_int64, C.c_int, C.c_int, _u8p,
+                                     _P(C.c_double)]
+        L.ref_oracle_build.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_uint64, C.c_int,
+                                       _f32p, _f32p, C.c_int64, C.c_int, C.c_int, _u8p]
+        L.ref_masked_attention.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, _f32p, _f32p, _f32p,
+                                           C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
+                                           _f32p]
+        L.ref_random_batch.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, _f32p, _f32p,
+                                       _f32p]
+        L.ref_frame_pair.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
+                                     _P(C.c_int64)]
+        L.ref_static_select.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
+                                        C.c_double, C.c_uint64, _P(C.c_int64), C.c_int64,
+                                        _P(C.c_int64)]
+        L.ref_proxy_scores.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
+                                       _f32p, _f32p, C.c_int64, C.c_int, C.c_int, _f32p,
+                                       _P(C.c_double), _P(C.c_double)]
+
+    def _chk(self, rc):
+        if rc != 0:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+
+    def build_mask(self, nf, nt, bs, cfg: Cfg, seed, disable_split=False, q=None, k=None,
+                   timings=None):
+        _, _, blocks, rb = grid_dims(nf, nt, bs)
+        out = np.zeros((blocks, rb), np.uint8)
+        q, k, tok, h, d = _feat(q, k)
+        t = (C.c_double * 5)()
+        c = cfg.c()
+        self._chk(self.lib.ref_build_mask(nf, nt, bs, C.byref(c), seed, int(disable_split),
+                                          _fp(q), _fp(k), tok, h, d,
+                                          out.ctypes.data_as(_u8p), t))
+        if timings is not None:
+            timings.update(candidates_s=t[0], selection_s=t[1], aggregation_s=t[2],
+                           retained_frame_pairs=int(t[3]), scored_pairs=int(t[4]))
+        return out
+
+    def oracle_build(self, nf, nt, bs, cfg: Cfg, seed, disable_split=False, q=None, k=None):
+        _, _, blocks, _ = grid_dims(nf, nt, bs)
+        out = np.zeros((blocks, blocks), np.uint8)
+        q, k, tok, h, d = _feat(q, k)
+        c = cfg.c()
+        self._chk(self.lib.ref_oracle_build(nf, nt, bs, C.byref(c), seed, int(disable_split),
+                                            _fp(q), _fp(k), tok, h, d,
+                                            out.ctypes.data_as(_u8p)))
+        return out
+
+    def masked_attention(self, nf, nt, bs, bits, q, k, v, exact=True, eps=1e-10):
+        _, padded, _, _ = grid_dims(nf, nt, bs)
+        q = np.ascontiguousarray(q, np.float32)
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        tok, h, d = q.shape
+        out = np.zeros((padded, h, d), np.float32)
+        bits = np.ascontiguousarray(bits, np.uint8)
+        self._chk(self.lib.ref_masked_attention(nf, nt, bs, bits.ctypes.data_as(_u8p), _fp(q),
+                                                _fp(k), _fp(v), tok, h, d, int(exact), eps,
+                                                _fp(out)))
+        return out
+
+    def random_batch(self, tokens, heads, d, seed, with_values=True):
+        q = np.zeros((tokens, heads, d), np.float32)
+        k = np.zeros_like(q)
+        v = np.zeros_like(q) if with_values else None
+        self._chk(self.lib.ref_random_batch(tokens, heads, d, seed, _fp(q), _fp(k), _fp(v)))
+        return q, k, v
+
+    def frame_pair(self, nf, nt, bs, cfg: Cfg, i, j):
+        out = (C.c_int64 * 5)()
+        c = cfg.c()
+        self._chk(self.lib.ref_frame_pair(nf, nt, bs, C.byref(c), i, j, out))
+        return tuple(out)
+
+    def static_select(self, nf, nt, bs, cfg: Cfg, i, j, ratio, seed):
+        n = self.frame_pair(nf, nt, bs, cfg, i, j)[2]
+        cap = max(1, n)
+        out = np.zeros((cap, 2), np.int64)
+        kk = C.c_int64()
+        c = cfg.c()
+        self._chk(self.lib.ref_static_select(nf, nt, bs, C.byref(c), i, j, ratio, seed,
+                                             out.ctypes.data_as(_P(C.c_int64)), cap,
+                                             C.byref(kk)))
+        return out[: kk.value]
+
+    def proxy_scores(self, nf, nt, bs, cfg: Cfg, i, j, q, k):
+        n = self.frame_pair(nf, nt, bs, cfg, i, j)[2]
+        q, k, tok, h, d = _feat(q, k)
+        s = np.zeros(max(n, 1), np.float32)
+        z = np.zeros(max(n, 1), np.float64)
+        st = (C.c_double * 2)()
+        c = cfg.c()
+        self._chk(self.lib.ref_proxy_scores(nf, nt, bs, C.byref(c), i, j, _fp(q), _fp(k), tok,
+                                            h, d, _fp(s), z.ctypes.data_as(_P(C.c_double)),
+                                            st))
+        return s[:n], z[:n], (st[0], st[1])
+
+
+class _PortLib(_Lib):
+    def __init__(self, path, kind):
+        super().__init__(path, kind)
+        L = self.lib
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_make_grid.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Grid)]
+        L.orc_frame_pair.argtypes = [_P(_Grid), _P(_Cfg), C.c_int, C.c_int, _P(C.c_int64)]
+        L.orc_build_mask.argtypes = [_P(_Grid), _P(_Cfg), C.c_uint64, C.c_int, _f32p, _f32p,
+                                     C.c_int64, C.c_int, C.c_int, _u8p, C.c_int,
+                                     _P(C.c_int64)]
+        L.orc_masked_attention_exact.argtypes = [_P(_Grid), _u8p, _f32p, _f32p, _f32p,
+                                                 C.c_int64, C.c_int, C.c_int, C.c_int64,
+                                                 C.c_int64, _f32p, C.c_int]
+        L.orc_random_batch.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, _f32p, _f32p,
+                                       _f32p, C.c_int]
+        L.orc_mix64.argtypes = [C.c_uint64]
+        L.orc_mix64.restype = C.c_uint64
+
+    def _grid(self, nf, nt, bs):
+        g = _Grid()
+        rc = self.lib.orc_make_grid(nf, nt, bs, C.byref(g))
+        if rc:
+            raise OracleError(rc, self.lib.orc_last_error().decode())
+        return g
+
+    def _chk(self, rc):
+        if rc != 0:
+            raise OracleError(rc, self.lib.orc_last_error().decode())
+
+    def frame_pair(self, nf, nt, bs, cfg: Cfg, i, j):
+        g = self._grid(nf, nt, bs)
+        out = (C.c_int64 * 5)()
+        c = cfg.c()
+        self.lib.orc_frame_pair(C.byref(g), C.byref(c), i, j, out)
+        return tuple(out)
+
+    def build_mask(self, nf, nt, bs, cfg: Cfg, seed, disable_split=False, q=None, k=None,
+                   threads=1, stats=None):
+        g = self._grid(nf, nt, bs)
+        out = np.zeros((g.blocks_per_dim, g.row_bytes), np.uint8)
+        q, k, tok, h, d = _feat(q, k)
+        st = (C.c_int64 * 2)()
+        c = cfg.c()
+        self._chk(self.lib.orc_build_mask(C.byref(g), C.byref(c), seed, int(disable_split),
+                                          _fp(q), _fp(k), tok, h, d,
+                                          out.ctypes.data_as(_u8p), threads, st))
+        if stats is not None:
+            stats.update(retained_frame_pairs=st[0], scored_pairs=st[1])
+        return out
+
+    def masked_attention_exact(self, nf, nt, bs, bits, q, k, v, row_begin=0, row_end=None,
+                               threads=1):
+        g = self._grid(nf, nt, bs)
+        if row_end is None:
+            row_end = g.padded_tokens
+        q = np.ascontiguousarray(q, np.float32)
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        tok, h, d = q.shape
+        out = np.zeros((row_end - row_begin, h, d), np.float32)
+        bits = np.ascontiguousarray(bits, np.uint8)
+        self._chk(self.lib.orc_masked_attention_exact(C.byref(g), bits.ctypes.data_as(_u8p),
+                                                      _fp(q), _fp(k), _fp(v), tok, h, d,
+                                                      row_begin, row_end, _fp(out), threads))
+        return out
+
+    def random_batch(self, tokens, heads, d, seed, with_values=True, threads=1):
+        q = np.zeros((tokens, heads, d), np.float32)
+        k = np.zeros_like(q)
+        v = np.zeros_like(q) if with_values else None
+        self.lib.orc_random_batch(tokens, heads, d, seed, _fp(q), _fp(k), _fp(v), threads)
+        return q, k, v
+
+    def mix64(self, z):
+        return self.lib.orc_mix64(z)
+
+
+# ---------------------------------------------------------------------------
+# Small pure-numpy helpers shared by tests (bit layout of BlockMask,
+# mask.hpp:17-35: row-major, LSB-first, row_bytes = ceil(S_b / 8)).
+
+def unpack_bits(bits, blocks):
+    return np.unpackbits(bits, axis=1, bitorder="little")[:, :blocks]
+
+
+def pack_dense(dense):
+    return np.packbits(dense.astype(np.uint8), axis=1, bitorder="little")

@@ -1,0 +1,409 @@
+// C-ABI entry points (include/dynrad.h): grid/config helpers, sparse
+// attention forward, mask utilities, host-buffer convenience.  The mask
+// builder entry points live in mask_build.cu.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+#include "plan.hpp"
+
+// Pull in the kernel definitions (single translation unit keeps template
+// instantiation and the launch sites together).
+#include "attn_f32.cu"
+#include "attn_sm100.cu"
+#include "csr.cu"
+
+namespace rp {
+
+static thread_local std::string t_err;
+std::atomic<long long> g_launches{0};
+void set_error(const std::string& msg) { t_err = msg; }
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw CudaError("no CUDA device available (dynrad has no CPU fallback)");
+}
+
+static int sm_count() {
+  int dev = 0, n = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  RP_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+// ------------------------------------------------------------ tensor maps --
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 3-D bf16 view {head_dim, heads, tokens} with a {64, 1, 128} box, 128B
+// swizzle; rows >= tokens read as zero (the reference's zero padding).
+static CUtensorMap make_map_bf16(const rp_tensor& t) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(t.head_dim), static_cast<cuuint64_t>(t.heads),
+                        static_cast<cuuint64_t>(t.tokens)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(t.head_stride) * 2,
+                           static_cast<cuuint64_t>(t.token_stride) * 2};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, t.data, dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+static void check_tensor(const rp_tensor* t, const char* name) {
+  if (!t || !t->data) throw std::invalid_argument(std::string("tensor ") + name + ": null");
+  if (t->tokens < 1 || t->heads < 1 || t->head_dim < 1)
+    throw std::invalid_argument("feature batch: empty dimensions");
+  if (t->dtype != RP_F32 && t->dtype != RP_BF16)
+    throw std::invalid_argument(std::string("tensor ") + name + ": dtype must be f32 or bf16");
+}
+
+static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tensor& k,
+                             const rp_tensor& v, rp_tensor& o, const int32_t* row_ptr,
+                             const int32_t* col_idx, const int32_t* row_order, float scale,
+                             cudaStream_t stream, int* err_flag) {
+  const int d = q.head_dim;
+  const float user_scale = scale;
+  if (scale <= 0.f) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  if (q.dtype == RP_BF16) {
+    if (g.block_size != 128)
+      throw std::invalid_argument("sparse attention (bf16): block_size must be 128");
+    if (d != 64 && d != 128)
+      throw std::invalid_argument("sparse attention (bf16): head_dim must be 64 or 128");
+    for (const rp_tensor* t : {&q, &k, &v, static_cast<const rp_tensor*>(&o)})
+      if (t->token_stride % 8 || t->head_stride % 8)
+        throw std::invalid_argument("sparse attention (bf16): strides must be multiples of 8");
+    const CUtensorMap mq = make_map_bf16(q), mk = make_map_bf16(k), mv = make_map_bf16(v);
+    attn::Params p;
+    p.row_ptr = row_ptr;
+    p.col_idx = col_idx;
+    p.row_order = row_order;
+    p.n_rows = static_cast<int>(g.blocks_per_dim);
+    p.heads = q.heads;
+    p.n_pairs = (q.heads + 1) / 2;
+    p.n_units = static_cast<long long>(p.n_pairs) * p.n_rows;
+    p.out = static_cast<__nv_bfloat16*>(o.data);
+    p.out_tok_stride = o.token_stride;
+    p.out_head_stride = o.head_stride;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
+    if (d == 128) {
+      static bool attr = false;
+      const int smem = attn::Layout<128>::kSmemBytes;
+      if (!attr) {
+        RP_CUDA(cudaFuncSetAttribute(attn::bsfa_fwd_kernel<128>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+      }
+      attn::bsfa_fwd_kernel<128><<<grid, attn::kThreads, smem, stream>>>(mq, mk, mv, p);
+    } else {
+      static bool attr = false;
+      const int smem = attn::Layout<64>::kSmemBytes;
+      if (!attr) {
+        RP_CUDA(cudaFuncSetAttribute(attn::bsfa_fwd_kernel<64>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+      }
+      attn::bsfa_fwd_kernel<64><<<grid, attn::kThreads, smem, stream>>>(mq, mk, mv, p);
+    }
+    RP_LAUNCHED();
+  } else {
+    if (d > attn32::kMaxD)
+      throw std::invalid_argument("sparse attention (f32): head_dim must be <= 128");
+    attn32::Params p;
+    p.q = static_cast<const float*>(q.data);
+    p.k = static_cast<const float*>(k.data);
+    p.v = static_cast<const float*>(v.data);
+    p.out = static_cast<float*>(o.data);
+    p.q_ts = q.token_stride; p.q_hs = q.head_stride;
+    p.k_ts = k.token_stride; p.k_hs = k.head_stride;
+    p.v_ts = v.token_stride; p.v_hs = v.head_stride;
+    p.o_ts = o.token_stride; p.o_hs = o.head_stride;
+    p.tokens = q.tokens;
+    p.padded = g.padded_tokens;
+    p.block = g.block_size;
+    p.heads = q.heads;
+    p.d = d;
+    p.row_ptr = row_ptr;
+    p.col_idx = col_idx;
+    p.scale = user_scale > 0.f ? static_cast<double>(user_scale)
+                               : 1.0 / std::sqrt(static_cast<double>(d));
+    p.error_flag = err_flag;
+    dim3 grid(static_cast<unsigned>((g.padded_tokens + attn32::kRows - 1) / attn32::kRows),
+              static_cast<unsigned>(q.heads));
+    attn32::attn_f32_kernel<<<grid, attn32::kThreads, 0, stream>>>(p);
+    RP_LAUNCHED();
+  }
+}
+
+static void launch_csr(const rp_grid& g, const uint8_t* bits, int32_t* row_ptr, int32_t* col_idx,
+                       int64_t col_cap, int32_t* row_order, int64_t* nnz, int32_t* counts,
+                       cudaStream_t stream) {
+  const int64_t n = g.blocks_per_dim;
+  const int threads = 256;
+  const unsigned warps_grid = static_cast<unsigned>((n * 32 + threads - 1) / threads);
+  csr::row_count_kernel<<<warps_grid, threads, 0, stream>>>(bits, n, g.row_bytes, counts);
+  RP_LAUNCHED();
+  csr::scan_kernel<<<1, 1024, 0, stream>>>(counts, n, row_ptr, nnz);
+  RP_LAUNCHED();
+  csr::fill_kernel<<<warps_grid, threads, 0, stream>>>(bits, n, g.row_bytes, row_ptr, col_idx,
+                                                       col_cap);
+  RP_LAUNCHED();
+  if (row_order) {
+    csr::order_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(counts, n,
+                                                                                  row_order);
+    RP_LAUNCHED();
+  }
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+const char* rp_last_error(void) { return t_err.c_str(); }
+const char* rp_version(void) { return "dynrad-b200 0.1 (sm_100a)"; }
+int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
+
+rp_status rp_make_grid(int nf, int nt, int bs, rp_grid* out) {
+  return guarded([&] {
+    rp_grid g{};
+    g.n_frames = nf;
+    g.tokens_per_frame = nt;
+    g.block_size = bs;
+    check_grid(&g);
+    g.total_tokens = static_cast<int64_t>(nf) * nt;
+    g.padded_tokens = (g.total_tokens + bs - 1) / bs * bs;
+    g.blocks_per_dim = g.padded_tokens / bs;
+    g.row_bytes = (g.blocks_per_dim + 7) / 8;
+    *out = g;
+  });
+}
+
+void rp_config_defaults(rp_config* c) {
+  c->mode = RP_STATIC_RATIO;
+  c->decay_factor = 1.0;
+  c->long_range_factor = 1.0;
+  c->split_epsilon = 1e-6;
+  c->mask_threshold = 0.75;
+  c->col_threshold = 0.20;
+  c->near_param = 0.25;
+  c->far_param = 0.55;
+  c->fallback_k = 1;
+}
+
+rp_status rp_config_validate(const rp_config* c) {
+  return guarded([&] { plan::validate(*c); });
+}
+
+rp_status rp_frame_pair_info(const rp_grid* g, const rp_config* c, int i, int j,
+                             rp_frame_pair* out) {
+  return guarded([&] {
+    check_grid(g);
+    if (i < 0 || j < 0 || i >= g->n_frames || j >= g->n_frames)
+      throw std::out_of_range("frame_pair: frame outside grid");
+    const int64_t t = std::llabs(static_cast<long long>(i) - j);
+    rp_frame_pair f{};
+    f.width = plan::window_width(i, j, *c, *g);
+    f.retained = plan::frame_retained(t, *c, *g) ? 1 : 0;
+    f.pair_count = f.retained ? plan::band_pairs(g->tokens_per_frame, f.width) : 0;
+    f.tier = plan::distance_tier(i, j, *c, *g);
+    f.split_factor = t >= 1 ? plan::split_factor(t, *c, *g) : 1;
+    if (c->mode == RP_STATIC_RATIO)
+      f.retention_or_threshold = f.tier == 0 ? 1.0 : (f.tier == 1 ? c->near_param : c->far_param);
+    else
+      f.retention_or_threshold = f.tier == 0 ? -std::numeric_limits<double>::infinity()
+                                             : (f.tier == 1 ? c->near_param : c->far_param);
+    *out = f;
+  });
+}
+
+rp_status rp_sparse_attention_fwd(const rp_grid* g, const rp_tensor* q, const rp_tensor* k,
+                                  const rp_tensor* v, rp_tensor* o, const int32_t* row_ptr,
+                                  const int32_t* col_idx, const int32_t* row_order,
+                                  float softmax_scale, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    check_tensor(q, "q");
+    check_tensor(k, "k");
+    check_tensor(v, "v");
+    check_tensor(o, "o");
+    if (k->tokens != q->tokens || v->tokens != q->tokens || k->heads != q->heads ||
+        v->heads != q->heads || k->head_dim != q->head_dim || v->head_dim != q->head_dim ||
+        k->dtype != q->dtype || v->dtype != q->dtype || o->dtype != q->dtype)
+      throw std::invalid_argument("feature batch: queries/keys/values shape mismatch");
+    if (g->padded_tokens < q->tokens)
+      throw std::invalid_argument("masked attention: mask smaller than batch");
+    if (o->tokens < g->padded_tokens || o->heads != q->heads || o->head_dim != q->head_dim)
+      throw std::invalid_argument("masked attention: output must be [S', heads, head_dim]");
+    if (!row_ptr || !col_idx) throw std::invalid_argument("masked attention: null row lists");
+    launch_attention(*g, *q, *k, *v, *o, row_ptr, col_idx, row_order, softmax_scale,
+                     reinterpret_cast<cudaStream_t>(stream), nullptr);
+  });
+}
+
+rp_status rp_mask_to_csr(const rp_grid* g, const uint8_t* bits, int32_t* row_ptr,
+                         int32_t* col_idx, int64_t col_cap, int32_t* row_order, int64_t* nnz,
+                         rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    if (!bits || !row_ptr || !col_idx) throw std::invalid_argument("mask_to_csr: null buffer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int32_t* counts = nullptr;
+    RP_CUDA(cudaMallocAsync(&counts, sizeof(int32_t) * (g->blocks_per_dim + 1), s));
+    launch_csr(*g, bits, row_ptr, col_idx, col_cap, row_order, nnz, counts, s);
+    RP_CUDA(cudaFreeAsync(counts, s));
+  });
+}
+
+rp_status rp_expand_mask(const rp_grid* g, const uint8_t* bits, uint8_t* token_bits,
+                         rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    const int64_t tok = g->padded_tokens, trb = (tok + 7) / 8;
+    const int64_t total = tok * trb;
+    csr::expand_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0,
+                         reinterpret_cast<cudaStream_t>(stream)>>>(
+        bits, g->blocks_per_dim, g->row_bytes, g->block_size, tok, trb, token_bits);
+    RP_LAUNCHED();
+  });
+}
+
+rp_status rp_mask_sparsity(const rp_grid* g, const uint8_t* bits, int64_t* active,
+                           double* sparsity, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long* d = nullptr;
+    RP_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), s));
+    RP_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
+    const int64_t n = g->blocks_per_dim * g->row_bytes;
+    csr::popcount_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024)), 256,
+                           0, s>>>(bits, n, d);
+    RP_LAUNCHED();
+    unsigned long long h = 0;
+    RP_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    RP_CUDA(cudaFreeAsync(d, s));
+    if (active) *active = static_cast<int64_t>(h);
+    if (sparsity)
+      *sparsity = 1.0 - static_cast<double>(h) /
+                            (static_cast<double>(g->blocks_per_dim) * g->blocks_per_dim);
+  });
+}
+
+rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_bits_host,
+                                         const void* q_host, const void* k_host,
+                                         const void* v_host, int dtype, int64_t tokens,
+                                         int heads, int head_dim, void* o_host,
+                                         rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    if (tokens < 1 || heads < 1 || head_dim < 1)
+      throw std::invalid_argument("feature batch: empty dimensions");
+    if (g->padded_tokens < tokens)
+      throw std::invalid_argument("masked attention: mask smaller than batch");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t es = dtype == RP_BF16 ? 2 : 4;
+    const size_t in_bytes = static_cast<size_t>(tokens) * heads * head_dim * es;
+    const size_t out_bytes = static_cast<size_t>(g->padded_tokens) * heads * head_dim * es;
+    const size_t mask_bytes = static_cast<size_t>(g->blocks_per_dim * g->row_bytes);
+    const int64_t nb = g->blocks_per_dim;
+    uint8_t *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr, *dm = nullptr;
+    int32_t *rp_ = nullptr, *ci = nullptr, *ro = nullptr, *cnt = nullptr;
+    int* flag = nullptr;
+    struct Free {
+      cudaStream_t s;
+      std::vector<void*> ptrs;
+      ~Free() {
+        for (void* p : ptrs)
+          if (p) cudaFreeAsync(p, s);
+      }
+    } fr{s, {}};
+    auto alloc = [&](auto** p, size_t b) {
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), b, s));
+      fr.ptrs.push_back(*p);
+    };
+    alloc(&dq, in_bytes);
+    alloc(&dk, in_bytes);
+    alloc(&dv, in_bytes);
+    alloc(&dout, out_bytes);
+    alloc(&dm, mask_bytes);
+    alloc(&rp_, sizeof(int32_t) * (nb + 1));
+    alloc(&ci, sizeof(int32_t) * nb * nb);
+    alloc(&ro, sizeof(int32_t) * nb);
+    alloc(&cnt, sizeof(int32_t) * (nb + 1));
+    alloc(&flag, sizeof(int));
+    RP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    RP_CUDA(cudaMemcpyAsync(dq, q_host, in_bytes, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(dk, k_host, in_bytes, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(dv, v_host, in_bytes, cudaMemcpyHostToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(dm, mask_bits_host, mask_bytes, cudaMemcpyHostToDevice, s));
+    launch_csr(*g, dm, rp_, ci, nb * nb, ro, nullptr, cnt, s);
+    // an empty row is a domain_error in the reference (attention.cpp:85-86)
+    std::vector<int32_t> hcnt(static_cast<size_t>(nb) + 1);
+    RP_CUDA(cudaMemcpyAsync(hcnt.data(), rp_, sizeof(int32_t) * (nb + 1),
+                            cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    for (int64_t r = 0; r < nb; ++r)
+      if (hcnt[r + 1] == hcnt[r]) throw std::domain_error("masked attention: row has no active key");
+    rp_tensor tq{dq, dtype, tokens, heads, head_dim, static_cast<int64_t>(heads) * head_dim,
+                 head_dim};
+    rp_tensor tk = tq, tv = tq;
+    tk.data = dk;
+    tv.data = dv;
+    rp_tensor to = tq;
+    to.data = dout;
+    to.tokens = g->padded_tokens;
+    launch_attention(*g, tq, tk, tv, to, rp_, ci, ro, 0.f, s, flag);
+    RP_CUDA(cudaMemcpyAsync(o_host, dout, out_bytes, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// Test support (not in the public header): run the UMMA descriptor probe.
+rp_status rp_debug_umma_probe(const void* A, const void* B, const void* P, const void* V,
+                              float* C1, float* C2, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int smem = 3 * 32768 + 1024;
+    RP_CUDA(cudaFuncSetAttribute(attn::umma_probe_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attn::umma_probe_kernel<<<1, 128, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(A), static_cast<const __nv_bfloat16*>(B),
+        static_cast<const __nv_bfloat16*>(P), static_cast<const __nv_bfloat16*>(V), C1, C2);
+    RP_LAUNCHED();
+  });
+}
+
+}  // extern "C"

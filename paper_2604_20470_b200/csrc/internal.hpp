@@ -1,0 +1,76 @@
+// Internal plumbing shared by the C-ABI translation units: exception ->
+// rp_status mapping (the reference's four exception types, mask.hpp /
+// selection.cpp / attention.cpp), CUDA error checking, launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+
+#include "dynrad.h"
+
+namespace rp {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_error(const std::string& msg);
+extern std::atomic<long long> g_launches;
+
+inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define RP_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      throw ::rp::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+#define RP_LAUNCHED()                                                              \
+  do {                                                                             \
+    ::rp::count_launch();                                                          \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      throw ::rp::CudaError(std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class F>
+rp_status guarded(F&& f) {
+  try {
+    f();
+    return RP_OK;
+  } catch (const CudaError& e) {
+    set_error(e.what());
+    return RP_CUDA_ERROR;
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return RP_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    set_error(e.what());
+    return RP_OUT_OF_RANGE;
+  } catch (const std::domain_error& e) {
+    set_error(e.what());
+    return RP_DOMAIN_ERROR;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return RP_RUNTIME_ERROR;
+  }
+}
+
+// Every compute entry point first checks that a CUDA device exists: the
+// product has no CPU fallback.
+void require_device();
+
+inline void check_grid(const rp_grid* g) {
+  if (!g) throw std::invalid_argument("grid: null");
+  if (g->n_frames < 1) throw std::invalid_argument("grid: n_frames must be >= 1");
+  if (g->tokens_per_frame < 1)
+    throw std::invalid_argument("grid: tokens_per_frame must be >= 1");
+  if (g->block_size < 2 || (g->block_size & (g->block_size - 1)))
+    throw std::invalid_argument("grid: block_size must be a power of two >= 2");
+}
+
+}  // namespace rp

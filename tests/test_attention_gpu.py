@@ -1,0 +1,143 @@
+"""Stage (d) parity: block-sparse attention on the B200 vs the reference.
+
+fp32 path: within 1e-5 (row-relative L2) of the reference's own
+masked_attention_exact (oracle/_ref, attention.cpp:50-121) on identical
+inputs, or of the C restatement (oracle/liboracle.so) where _ref is absent.
+bf16 path: within 2e-2 of an fp32 evaluation on the same bf16-rounded inputs
+(torch fp32 on the GPU for mid sizes, the oracle at small sizes).
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_rows
+from oracle import pyoracle
+from paper_2604_20470_b200 import radialplan as rp
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16_round(x):
+    return torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+
+
+def _random_mask(nb, density, seed):
+    rng = np.random.default_rng(seed)
+    dense = (rng.random((nb, nb)) < density).astype(np.uint8)
+    np.fill_diagonal(dense, 1)
+    return dense
+
+
+def _torch_ref(q, k, v, dense, B, S):
+    """fp32 dense masked attention over the padded axis (zero pad rows)."""
+    Sp = dense.shape[0] * B
+    H, d = q.shape[1], q.shape[2]
+    def pad(x):
+        y = torch.zeros((Sp, H, d), dtype=torch.float32, device="cuda")
+        y[:S] = x.float()
+        return y
+    qp, kp, vp = pad(q), pad(k), pad(v)
+    tok = torch.from_numpy(np.kron(dense, np.ones((B, B), np.uint8))).cuda().bool()
+    out = torch.empty((Sp, H, d), dtype=torch.float32, device="cuda")
+    for h in range(H):
+        s = (qp[:, h] @ kp[:, h].T) / np.sqrt(d)
+        s = s.masked_fill(~tok, float("-inf"))
+        out[:, h] = torch.softmax(s, dim=-1) @ vp[:, h]
+    return out
+
+
+def test_umma_descriptor_probe(cuda):
+    """Pins the smem/TMEM operand conventions the tcgen05 kernels rely on."""
+    import ctypes as C
+    from paper_2604_20470_b200 import _lib
+    g = torch.Generator(device="cpu").manual_seed(0)
+    A, B, P, V = (torch.randn(128, 128, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
+    C1 = torch.zeros(128, 128, device="cuda")
+    C2 = torch.zeros(128, 128, device="cuda")
+    _lib.check(_lib.lib().rp_debug_umma_probe(*(C.c_void_p(t.data_ptr()) for t in (A, B, P, V, C1, C2)),
+                                              C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    e1 = A.float() @ B.float().T
+    e2 = P.float() @ V.float()
+    assert torch.allclose(C1, e1, rtol=1e-3, atol=1e-2), (C1 - e1).abs().max()
+    assert torch.allclose(C2, e2, rtol=1e-3, atol=1e-2), (C2 - e2).abs().max()
+
+
+@pytest.mark.parametrize("nf,nt,heads,d,density", [
+    (4, 300, 3, 128, 0.5),   # padded last block, odd heads (single-tile unit)
+    (4, 300, 2, 64, 0.4),
+    (8, 640, 4, 128, 0.35),  # 40 block rows: long KV lists, ring wrap-around
+    (2, 128, 2, 128, 1.0),   # dense
+])
+def test_bf16_kernel_vs_fp32(cuda, nf, nt, heads, d, density):
+    g = rp.make_grid(nf, nt, 128)
+    S = g.total_tokens
+    torch.manual_seed(1)
+    q = torch.randn(S, heads, d, device="cuda").to(torch.bfloat16)
+    k = torch.randn(S, heads, d, device="cuda").to(torch.bfloat16)
+    v = torch.randn(S, heads, d, device="cuda").to(torch.bfloat16)
+    dense = _random_mask(g.blocks_per_dim, density, nf * 7 + d)
+    bits = pyoracle.pack_dense(dense)
+    mdev = torch.from_numpy(bits).cuda()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mdev)
+    out = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order)
+    torch.cuda.synchronize()
+    ref = _torch_ref(q, k, v, dense, 128, S)
+    err = rel_rows(out.float().cpu().numpy(), ref.cpu().numpy())
+    assert err < 2e-2, err
+
+
+def test_csr_matches_bitmask(cuda):
+    g = rp.make_grid(5, 1000, 128)
+    dense = _random_mask(g.blocks_per_dim, 0.3, 3)
+    mdev = torch.from_numpy(pyoracle.pack_dense(dense)).cuda()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mdev)
+    rp_ = row_ptr.cpu().numpy()
+    ci = col_idx.cpu().numpy()
+    for r in range(g.blocks_per_dim):
+        assert list(ci[rp_[r]:rp_[r + 1]]) == list(np.nonzero(dense[r])[0])
+    nnz = dense.sum(1)
+    o = order.cpu().numpy()
+    assert sorted(o.tolist()) == list(range(g.blocks_per_dim))
+    assert all(nnz[o[i]] > nnz[o[i + 1]] or (nnz[o[i]] == nnz[o[i + 1]] and o[i] < o[i + 1])
+               for i in range(len(o) - 1))
+
+
+@pytest.mark.parametrize("bs", [32, 64, 128])
+def test_fp32_path_vs_reference(cuda, bs):
+    """tiny config: 8 x 256 tokens, 2 heads, d=64 (BASELINE configs[0])."""
+    P = pyoracle.port()
+    q, k, v = P.random_batch(2048, 2, 64, 42, threads=4)
+    cfg = pyoracle.Cfg(0, 2.0, 0.3, 1e-6, 0.75, 0.2, 0.2, 0.2)
+    bits = P.build_mask(8, 256, bs, cfg, 7)
+    g = rp.make_grid(8, 256, bs)
+    out = rp.masked_attention_exact(g, rp.BlockMask(g.blocks_per_dim, bits), q, k, v)
+    if pyoracle.have_ref():
+        ref = pyoracle.ref().masked_attention(8, 256, bs, bits, q, k, v)
+    else:
+        ref = P.masked_attention_exact(8, 256, bs, bits, q, k, v, threads=8)
+    assert rel_rows(out, ref) < 1e-5
+
+
+def test_fp32_padding_semantics(cuda):
+    """8 x 250 tokens at B=32: padded keys are attended (attention.cpp:43-48)."""
+    P = pyoracle.port()
+    q, k, v = P.random_batch(2000, 2, 32, 5, threads=4)
+    cfg = pyoracle.Cfg(0, 1.0, 1.0, 1e-6, 0.75, 0.2, 0.22, 0.22)
+    bits = P.build_mask(8, 250, 32, cfg, 7)
+    g = rp.make_grid(8, 250, 32)
+    out = rp.masked_attention_exact(g, rp.BlockMask(g.blocks_per_dim, bits), q, k, v)
+    ref = P.masked_attention_exact(8, 250, 32, bits, q, k, v, threads=8)
+    assert out.shape == (2016, 2, 32)
+    assert rel_rows(out, ref) < 1e-5
+
+
+def test_fp32_empty_row_is_domain_error(cuda):
+    g = rp.make_grid(2, 64, 32)
+    m = rp.BlockMask(g.blocks_per_dim)
+    m.set(0, 0)
+    m.set(1, 1)
+    m.set(2, 2)  # row 3 empty
+    q = np.ones((128, 1, 8), np.float32)
+    with pytest.raises(rp.DomainError):
+        rp.masked_attention_exact(g, m, q, q, q)
