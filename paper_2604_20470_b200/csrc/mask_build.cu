@@ -1,37 +1,798 @@
-// Mask builder entry points (stub; filled in by the next milestone).
+// Stages (a)-(c) on the GPU: radialplan::build_mask (mask.cpp:162-289).
+//
+// Host side plans the frame-pair job table (plan.hpp, O(N_f^2) scalars with
+// the reference's exact arithmetic).  Device side does all per-token / per-
+// pair work:
+//   K1  base mask: intra-frame rectangles (mask.cpp:175-183) and full-band
+//       pairs (ratio >= 1 or tau = -inf) by closed-form column counts
+//       (mask.cpp:132-158) -> theta_c / theta_m rule -> atomicOr.
+//   K4  static ratio: exact partial Fisher-Yates (mask.cpp:224-252) resolved
+//       in parallel: counter-form splitmix64 draws, a radix sort of
+//       (pair, target, step) keys, then a pointer chase that recovers the
+//       value each step swaps into its slot; per-column counts by atomics.
+//   K2/K3 dynamic threshold, exact engine: fp64 token-pair proxy scores with
+//       the reference's pinned operation order (selection.cpp:93-123),
+//       sequential per-pair mean / population std (selection.cpp:125-148),
+//       z >= tau, fallback_k best (selection.cpp:150-185).  The tensor-core
+//       engine for large grids lives in mask_score_sm100.cu.
+// Per-frame-pair counts are never merged across pairs (a tile straddling two
+// frame pairs is judged per pair and OR-ed, mask.cpp:87-125).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
 #include "internal.hpp"
+#include "mask_build.cuh"
 #include "plan.hpp"
 
-using namespace rp;
+namespace rp {
+namespace mask {
 
-struct rp_plan_s {
-  rp_grid g;
-  rp_config c;
-  uint64_t seed;
-  rp_build_options o;
+// ------------------------------------------------------------ helpers -----
+RP_DEV void set_block(uint32_t* words, int64_t row_bytes, int64_t r, int64_t c) {
+  const int64_t byte = r * row_bytes + c / 8;
+  atomicOr(&words[byte >> 2], 1u << (((byte & 3) << 3) + (c & 7)));
+}
+
+// Offsets of the canonical row-major band enumeration (radial.cpp:64-79) in
+// closed form: off(u) = sum_{x<u} (min(N-1, x+w) - max(0, x-w) + 1).
+RP_HD int64_t band_off(int64_t u, int64_t N, int64_t w) {
+  int64_t a = N - w;
+  if (a < 0) a = 0;
+  if (a > u) a = u;
+  const int64_t hi = a * (a - 1) / 2 + a * w + (u - a) * (N - 1);
+  int64_t c = u - 1 - w;
+  if (c < 0) c = 0;
+  return hi - c * (c + 1) / 2 + u;
+}
+// Flat index -> (u, v): largest u with off(u) <= flat (upper_bound - 1).
+RP_HD void band_uv(int64_t flat, int64_t N, int64_t w, int64_t* u, int64_t* v) {
+  int64_t lo = 0, hi = N;  // off(lo) <= flat < off(hi)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (band_off(mid, N, w) <= flat) lo = mid; else hi = mid;
+  }
+  *u = lo;
+  *v = (lo - w > 0 ? lo - w : 0) + (flat - band_off(lo, N, w));
+}
+
+// ---------------------------------------------------- K1: base mask -------
+__global__ void intra_kernel(uint32_t* words, int nf, int64_t nt, int bs, int64_t row_bytes,
+                             int span) {
+  const int f = blockIdx.x;
+  const int64_t lo = static_cast<int64_t>(f) * nt, hi = lo + nt - 1;
+  const int64_t b0 = lo / bs, b1 = hi / bs;
+  for (int x = threadIdx.x; x < span * span; x += blockDim.x) {
+    const int64_t r = b0 + x / span, c = b0 + x % span;
+    if (r <= b1 && c <= b1) set_block(words, row_bytes, r, c);
+  }
+}
+
+// Per (job, tile) item with B (<= 1024) threads: one column each.
+// mode 0: closed-form full-band counts; mode 1: counts from a buffer.
+__global__ void apply_kernel(const DJob* __restrict__ jobs, const Item* __restrict__ items,
+                             const uint32_t* __restrict__ counts, uint32_t* words, int64_t nt,
+                             int bs, int64_t row_bytes, int cmin, int amin, int mode) {
+  const Item it = items[blockIdx.x];
+  const DJob& jb = jobs[it.job];
+  __shared__ int active;
+  if (threadIdx.x == 0) active = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int k = threadIdx.x; k < bs; k += blockDim.x) {
+    uint32_t cnt = 0;
+    if (mode == 0) {
+      // mask.cpp:132-158: column v of frame j hit by rows [v-w, v+w] of frame i
+      const int64_t qi = static_cast<int64_t>(jb.i) * nt, kj = static_cast<int64_t>(jb.j) * nt;
+      const int64_t gc = (jb.c0 + it.tc) * bs + k;
+      const int64_t lv = gc - kj;
+      if (lv >= 0 && lv < nt) {
+        const int64_t ulo = lv - jb.width > 0 ? lv - jb.width : 0;
+        const int64_t uhi = lv + jb.width < nt - 1 ? lv + jb.width : nt - 1;
+        const int64_t R0 = (jb.r0 + it.tr) * bs, R1 = R0 + bs - 1;
+        const int64_t lo = qi + ulo > R0 ? qi + ulo : R0;
+        const int64_t hi = qi + uhi < R1 ? qi + uhi : R1;
+        if (ulo <= uhi && lo <= hi) cnt = static_cast<uint32_t>(hi - lo + 1);
+      }
+    } else {
+      cnt = counts[jb.cnt_off + (static_cast<int64_t>(it.tr) * jb.tc + it.tc) * bs + k];
+    }
+    mine += cnt >= static_cast<uint32_t>(cmin);
+  }
+  if (mine) atomicAdd(&active, mine);
+  __syncthreads();
+  if (threadIdx.x == 0 && active >= amin)
+    set_block(words, row_bytes, jb.r0 + it.tr, jb.c0 + it.tc);
+}
+
+RP_DEV void add_count(const DJob& jb, uint32_t* counts, int64_t nt, int bs, int64_t u,
+                      int64_t v) {
+  const int64_t gr = static_cast<int64_t>(jb.i) * nt + u;
+  const int64_t gc = static_cast<int64_t>(jb.j) * nt + v;
+  const int64_t rr = gr / bs - jb.r0, cc = gc / bs - jb.c0;
+  atomicAdd(&counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs], 1u);
+}
+
+RP_DEV int find_job(const int64_t* __restrict__ off, int n_jobs, int64_t x) {
+  int lo = 0, hi = n_jobs;  // off[lo] <= x < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------ K4: exact partial Fisher-Yates --
+// Draw d of job j: r_d = d + next_d % (n - d), next_d = stream call d of
+// SplitMix64(pair_seed) (rng.hpp:40-48, mask.cpp:245-248).
+RP_DEV int64_t fy_target(const DJob& jb, int64_t d) {
+  const uint64_t x = stream_at(jb.seed, static_cast<uint64_t>(d));
+  return d + static_cast<int64_t>(x % static_cast<uint64_t>(jb.n - d));
+}
+
+__global__ void fy_draw_kernel(const DJob* __restrict__ jobs, const int* __restrict__ batch_jobs,
+                               const int64_t* __restrict__ off, int n_jobs, int64_t total,
+                               int bits, uint64_t* __restrict__ keys) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= total) return;
+  const int lj = find_job(off, n_jobs, x);
+  const DJob& jb = jobs[batch_jobs[lj]];
+  const int64_t d = x - off[lj];
+  const int64_t r = fy_target(jb, d);
+  keys[x] = (static_cast<uint64_t>(lj) << (2 * bits)) | (static_cast<uint64_t>(r) << bits) |
+            static_cast<uint64_t>(d);
+}
+
+// After sorting by (job, target, step): prev[d] = previous step with the same
+// target (or -1); tlast[p] (p < k) = last step e != p that targeted slot p.
+__global__ void fy_link_kernel(const uint64_t* __restrict__ keys, int64_t total, int bits,
+                               const int64_t* __restrict__ off, int32_t* __restrict__ prev,
+                               int32_t* __restrict__ tlast, const DJob* __restrict__ jobs,
+                               const int* __restrict__ batch_jobs) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const uint64_t mask = (uint64_t{1} << bits) - 1;
+  const uint64_t key = keys[i];
+  const uint64_t grp = key >> bits;  // (job, target)
+  const int lj = static_cast<int>(key >> (2 * bits));
+  const int64_t r = static_cast<int64_t>((key >> bits) & mask);
+  const int64_t d = static_cast<int64_t>(key & mask);
+  const bool has_prev = i > 0 && (keys[i - 1] >> bits) == grp;
+  const int64_t dprev = has_prev ? static_cast<int64_t>(keys[i - 1] & mask) : -1;
+  prev[off[lj] + d] = static_cast<int32_t>(dprev);
+  const bool last = i + 1 == total || (keys[i + 1] >> bits) != grp;
+  const int64_t k = jobs[batch_jobs[lj]].k;
+  if (last && r < k) {
+    const int64_t e = d != r ? d : dprev;  // exclude the slot's own step
+    tlast[off[lj] + r] = static_cast<int32_t>(e);
+  }
+}
+
+// Value swapped into slot d at step d, then counted into its tile column.
+__global__ void fy_count_kernel(const DJob* __restrict__ jobs, const int* __restrict__ batch_jobs,
+                                const int64_t* __restrict__ off, int n_jobs, int64_t total,
+                                const int32_t* __restrict__ prev,
+                                const int32_t* __restrict__ tlast, uint32_t* counts, int64_t nt,
+                                int bs) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= total) return;
+  const int lj = find_job(off, n_jobs, x);
+  const DJob& jb = jobs[batch_jobs[lj]];
+  const int64_t d = x - off[lj];
+  const int32_t* tl = tlast + off[lj];
+  int64_t val;
+  const int32_t p = prev[x];
+  if (p < 0) {
+    val = fy_target(jb, d);  // slot r_d untouched before step d
+  } else {
+    // A(e): value at slot e before step e = A(tlast[e]) chased down.
+    int64_t e = p;
+    while (tl[e] >= 0) e = tl[e];
+    val = e;
+  }
+  int64_t u, v;
+  band_uv(val, nt, jb.width, &u, &v);
+  add_count(jb, counts, nt, bs, u, v);
+}
+
+// ------------------------------------ K2/K3 exact engine (fp64 SIMT) -------
+struct Feat {
+  const void* q;
+  const void* k;
+  int dtype;
+  int64_t q_ts, q_hs, k_ts, k_hs;
+  int heads, d;
+  double inv_sqrt_d;
 };
 
+RP_DEV float feat_at(const void* p, int dtype, int64_t idx) {
+  return dtype == RP_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[idx])
+                          : static_cast<const float*>(p)[idx];
+}
+
+// selection.cpp:104-121: per-head dot in double (ascending d), acc +=
+// dot * inv_sqrt_d (no contraction), float(acc / heads).
+RP_DEV float exact_score(const Feat& f, int64_t qrow, int64_t krow) {
+  double acc = 0.0;
+  for (int h = 0; h < f.heads; ++h) {
+    const int64_t qb = qrow * f.q_ts + h * f.q_hs, kb = krow * f.k_ts + h * f.k_hs;
+    double dot = 0.0;
+    for (int e = 0; e < f.d; ++e)
+      dot = __fma_rn(static_cast<double>(feat_at(f.q, f.dtype, qb + e)),
+                     static_cast<double>(feat_at(f.k, f.dtype, kb + e)), dot);
+    acc = __dadd_rn(acc, __dmul_rn(dot, f.inv_sqrt_d));
+  }
+  return __double2float_rn(__ddiv_rn(acc, static_cast<double>(f.heads)));
+}
+
+__global__ void exact_scores_kernel(const DJob* __restrict__ jobs,
+                                    const int* __restrict__ batch_jobs,
+                                    const int64_t* __restrict__ off, int n_jobs, int64_t total,
+                                    Feat f, int64_t nt, float* __restrict__ scores) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= total) return;
+  const int lj = find_job(off, n_jobs, x);
+  const DJob& jb = jobs[batch_jobs[lj]];
+  int64_t u, v;
+  band_uv(x - off[lj], nt, jb.width, &u, &v);
+  scores[x] = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
+                          static_cast<int64_t>(jb.j) * nt + v);
+}
+
+// selection.cpp:133-142, sequential like the reference: bit-identical stats.
+__global__ void seq_stats_kernel(const int64_t* __restrict__ off, int n_jobs,
+                                 const float* __restrict__ scores, double2* __restrict__ stats) {
+  const int lj = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lj >= n_jobs) return;
+  const float* s = scores + off[lj];
+  const int64_t n = off[lj + 1] - off[lj];
+  double sum = 0.0;
+  for (int64_t x = 0; x < n; ++x) sum = __dadd_rn(sum, static_cast<double>(s[x]));
+  const double mean = __ddiv_rn(sum, static_cast<double>(n));
+  double sq = 0.0;
+  for (int64_t x = 0; x < n; ++x) {
+    const double dd = __dsub_rn(static_cast<double>(s[x]), mean);
+    sq = __dadd_rn(sq, __dmul_rn(dd, dd));
+  }
+  stats[lj] = make_double2(mean, __dsqrt_rn(__ddiv_rn(sq, static_cast<double>(n))));
+}
+
+RP_DEV double zscore(float s, double2 st) {
+  return __ddiv_rn(__dsub_rn(static_cast<double>(s), st.x), __dadd_rn(st.y, 1e-8));
+}
+
+__global__ void exact_select_kernel(const DJob* __restrict__ jobs,
+                                    const int* __restrict__ batch_jobs,
+                                    const int64_t* __restrict__ off, int n_jobs, int64_t total,
+                                    const float* __restrict__ scores,
+                                    const double2* __restrict__ stats, uint32_t* counts,
+                                    unsigned long long* kept, int64_t nt, int bs) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= total) return;
+  const int lj = find_job(off, n_jobs, x);
+  const DJob& jb = jobs[batch_jobs[lj]];
+  if (zscore(scores[x], stats[lj]) >= jb.param) {
+    int64_t u, v;
+    band_uv(x - off[lj], nt, jb.width, &u, &v);
+    add_count(jb, counts, nt, bs, u, v);
+    atomicAdd(&kept[lj], 1ull);
+  }
+}
+
+// selection.cpp:163-175: if nothing cleared tau keep the fallback_k best z,
+// ties to the lowest flat index.  One CTA per job; k rounds of argmax.
+__global__ void exact_fallback_kernel(const DJob* __restrict__ jobs,
+                                      const int* __restrict__ batch_jobs,
+                                      const int64_t* __restrict__ off,
+                                      const float* __restrict__ scores,
+                                      const double2* __restrict__ stats,
+                                      const unsigned long long* __restrict__ kept,
+                                      uint32_t* counts, int64_t nt, int bs, int fallback_k,
+                                      unsigned long long* n_fallback) {
+  const int lj = blockIdx.x;
+  if (kept[lj] != 0) return;
+  const DJob& jb = jobs[batch_jobs[lj]];
+  const int64_t n = off[lj + 1] - off[lj];
+  const float* s = scores + off[lj];
+  const double2 st = stats[lj];
+  __shared__ double bz[32];
+  __shared__ int64_t bi[32];
+  __shared__ int64_t last_pick;
+  __shared__ double last_z;
+  const int k = static_cast<int>(fallback_k < n ? fallback_k : n);
+  if (threadIdx.x == 0) {
+    last_pick = -1;
+    last_z = INFINITY;
+    atomicAdd(n_fallback, 1ull);
+  }
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    // best (z, -index) strictly after (last_z, last_pick) in the order
+    // z descending then index ascending.
+    double best = -INFINITY;
+    int64_t besti = -1;
+    for (int64_t x = threadIdx.x; x < n; x += blockDim.x) {
+      const double z = zscore(s[x], st);
+      const bool after = z < last_z || (z == last_z && x > last_pick);
+      if (!after) continue;
+      if (besti < 0 || z > best || (z == best && x < besti)) {
+        best = z;
+        besti = x;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oz = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xFFFFFFFFu, besti, o);
+      if (oi >= 0 && (besti < 0 || oz > best || (oz == best && oi < besti))) {
+        best = oz;
+        besti = oi;
+      }
+    }
+    if (threadIdx.x % 32 == 0) {
+      bz[threadIdx.x / 32] = best;
+      bi[threadIdx.x / 32] = besti;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
+        if (bi[w] >= 0 && (bi[0] < 0 || bz[w] > bz[0] || (bz[w] == bz[0] && bi[w] < bi[0]))) {
+          bz[0] = bz[w];
+          bi[0] = bi[w];
+        }
+      if (bi[0] >= 0) {
+        int64_t u, v;
+        band_uv(bi[0], nt, jb.width, &u, &v);
+        add_count(jb, counts, nt, bs, u, v);
+      }
+      last_pick = bi[0];
+      last_z = bz[0];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace mask
+}  // namespace rp
+
+// =========================================================================
+using namespace rp;
+using namespace rp::mask;
+
+namespace {
+
+// Device buffer: stream-ordered (temporaries of one build) or, with
+// persistent = true, a plain allocation owned by a plan.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  bool persistent = false;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t st, bool keep = false) : n(count), s(st), persistent(keep) {
+    if (!count) return;
+    if (keep) RP_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count));
+    else RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, st));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), persistent(o.persistent) {
+    o.p = nullptr;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(s, o.s);
+    std::swap(persistent, o.persistent);
+    return *this;
+  }
+  ~DevBuf() {
+    if (!p) return;
+    if (persistent) cudaFree(p);
+    else cudaFreeAsync(p, s);
+  }
+  void upload(const T* h, size_t count) {
+    RP_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  }
+};
+
+int bit_length(uint64_t x) {
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+}  // namespace
+
+struct rp_plan_s {
+  rp_grid g{};
+  rp_config c{};
+  uint64_t seed = 0;
+  rp_build_options o{};
+  std::vector<plan::Job> jobs;
+  std::vector<DJob> djobs;
+  int cmin = 0, amin = 0;
+  size_t words = 0;  // 32-bit words of the padded mask buffer
+  // device state (allocated with the stream of the first build)
+  cudaStream_t s = nullptr;
+  DevBuf<DJob> d_jobs;
+  DevBuf<uint32_t> base;    // intra-frame + full-band bits
+  DevBuf<uint32_t> cached;  // static mode: the full mask
+  bool base_ready = false, static_ready = false;
+  int64_t retained = 0, sampled = 0, scored = 0;
+};
+
+namespace {
+
+void make_jobs(rp_plan_s& P) {
+  const rp_grid& g = P.g;
+  const rp_config& c = P.c;
+  const int64_t nt = g.tokens_per_frame;
+  for (int i = 0; i < g.n_frames; ++i)
+    for (int j = 0; j < g.n_frames; ++j) {
+      const int64_t t = std::llabs(static_cast<long long>(i) - j);
+      if (t < 1) continue;
+      const bool ret = plan::frame_retained(t, c, g);
+      if (!P.o.disable_split && !ret) continue;
+      plan::Job jb{};
+      jb.i = i;
+      jb.j = j;
+      jb.tier = plan::distance_tier(i, j, c, g);
+      jb.width = plan::window_width(i, j, c, g);
+      jb.n = ret ? plan::band_pairs(nt, jb.width) : 0;
+      jb.stream_seed = pair_seed(P.seed, i, j);
+      if (c.mode == RP_STATIC_RATIO) {
+        jb.param = jb.tier == 0 ? 1.0 : (jb.tier == 1 ? c.near_param : c.far_param);
+        if (jb.param >= 1.0) {
+          jb.kind = plan::kFullBand;
+        } else {
+          if (jb.n == 0)
+            throw std::invalid_argument(
+                "build_mask: disable_split samples a pruned frame pair (empty candidate set; "
+                "the reference divides by zero here)");
+          jb.kind = plan::kSample;
+          jb.k = static_cast<int64_t>(std::floor(static_cast<double>(jb.n) * jb.param));
+          if (jb.k < 1) jb.k = 1;
+        }
+      } else {
+        jb.param = jb.tier == 0 ? -std::numeric_limits<double>::infinity()
+                                : (jb.tier == 1 ? c.near_param : c.far_param);
+        if (jb.tier == 0) jb.kind = plan::kFullBand;
+        else jb.kind = jb.n > 0 ? plan::kScore : plan::kEmpty;
+      }
+      P.jobs.push_back(jb);
+    }
+  const int bs = g.block_size;
+  for (const plan::Job& jb : P.jobs) {
+    DJob d{};
+    d.i = jb.i;
+    d.j = jb.j;
+    d.kind = jb.kind;
+    d.width = jb.width;
+    d.n = jb.n;
+    d.k = jb.k;
+    d.param = jb.param;
+    d.seed = jb.stream_seed;
+    const int64_t qi = static_cast<int64_t>(jb.i) * nt, kj = static_cast<int64_t>(jb.j) * nt;
+    d.r0 = static_cast<int32_t>(qi / bs);
+    d.c0 = static_cast<int32_t>(kj / bs);
+    d.tr = static_cast<int32_t>((qi + nt - 1) / bs - d.r0 + 1);
+    d.tc = static_cast<int32_t>((kj + nt - 1) / bs - d.c0 + 1);
+    P.djobs.push_back(d);
+  }
+  P.cmin = plan::count_threshold(c.col_threshold, bs);
+  P.amin = plan::count_threshold(c.mask_threshold, bs);
+  P.retained = static_cast<int64_t>(P.jobs.size());
+}
+
+int apply_threads(int bs) { return bs >= 1024 ? 1024 : (bs < 32 ? 32 : bs); }
+
+void launch_apply(rp_plan_s& P, const std::vector<Item>& items, const uint32_t* counts,
+                  uint32_t* words, int mode, cudaStream_t s) {
+  if (items.empty()) return;
+  DevBuf<Item> d_items(items.size(), s);
+  d_items.upload(items.data(), items.size());
+  const int64_t chunk = 1 << 30;  // grid.x limit safety
+  for (int64_t b = 0; b < static_cast<int64_t>(items.size()); b += chunk) {
+    const int64_t nb = std::min<int64_t>(chunk, items.size() - b);
+    apply_kernel<<<static_cast<unsigned>(nb), apply_threads(P.g.block_size), 0, s>>>(
+        P.d_jobs.p, d_items.p + b, counts, words, P.g.tokens_per_frame, P.g.block_size,
+        P.g.row_bytes, P.cmin, P.amin, mode);
+    RP_LAUNCHED();
+  }
+}
+
+void tiles_of(const rp_plan_s& P, int job, std::vector<Item>& out) {
+  const DJob& d = P.djobs[job];
+  for (int32_t r = 0; r < d.tr; ++r)
+    for (int32_t c = 0; c < d.tc; ++c) out.push_back(Item{job, r, c});
+}
+
+// Intra-frame rectangles + every full-band pair, once per plan.
+void build_base(rp_plan_s& P, cudaStream_t s) {
+  const rp_grid& g = P.g;
+  P.base = DevBuf<uint32_t>(P.words, s, true);
+  RP_CUDA(cudaMemsetAsync(P.base.p, 0, P.words * 4, s));
+  const int span = static_cast<int>((g.tokens_per_frame + g.block_size - 1) / g.block_size + 1);
+  intra_kernel<<<g.n_frames, 256, 0, s>>>(P.base.p, g.n_frames, g.tokens_per_frame,
+                                          g.block_size, g.row_bytes, span);
+  RP_LAUNCHED();
+  std::vector<Item> items;
+  for (int jx = 0; jx < static_cast<int>(P.djobs.size()); ++jx)
+    if (P.djobs[jx].kind == plan::kFullBand) tiles_of(P, jx, items);
+  launch_apply(P, items, nullptr, P.base.p, 0, s);
+  P.base_ready = true;
+}
+
+// Batches of jobs of one kind whose per-job sizes (`size(job)`) sum to at
+// most `cap` elements (a single oversized job forms its own batch).
+template <class F>
+std::vector<std::vector<int>> batches(const rp_plan_s& P, int kind, int64_t cap, F size) {
+  std::vector<std::vector<int>> out;
+  std::vector<int> cur;
+  int64_t tot = 0;
+  for (int jx = 0; jx < static_cast<int>(P.djobs.size()); ++jx) {
+    if (P.djobs[jx].kind != kind) continue;
+    const int64_t sz = size(P.djobs[jx]);
+    if (!cur.empty() && tot + sz > cap) {
+      out.push_back(cur);
+      cur.clear();
+      tot = 0;
+    }
+    cur.push_back(jx);
+    tot += sz;
+  }
+  if (!cur.empty()) out.push_back(cur);
+  return out;
+}
+
+// Count buffers for a batch: one [tr][tc][B] block per job.
+int64_t assign_counts(rp_plan_s& P, const std::vector<int>& batch) {
+  int64_t off = 0;
+  for (int jx : batch) {
+    P.djobs[jx].cnt_off = off;
+    off += static_cast<int64_t>(P.djobs[jx].tr) * P.djobs[jx].tc * P.g.block_size;
+  }
+  return off;
+}
+
+constexpr int64_t kDrawCap = int64_t{1} << 28;   // draws per static batch
+constexpr int64_t kScoreCap = int64_t{1} << 29;  // scores per exact batch
+
+void build_static(rp_plan_s& P, uint32_t* words, cudaStream_t s) {
+  const int bs = P.g.block_size;
+  const int64_t nt = P.g.tokens_per_frame;
+  auto bl = batches(P, plan::kSample, kDrawCap, [](const DJob& d) { return d.k; });
+  for (auto& batch : bl) {
+    const int nj = static_cast<int>(batch.size());
+    std::vector<int64_t> off(nj + 1, 0);
+    int64_t max_n = 1;
+    for (int x = 0; x < nj; ++x) {
+      off[x + 1] = off[x] + P.djobs[batch[x]].k;
+      max_n = std::max(max_n, P.djobs[batch[x]].n);
+    }
+    const int64_t total = off[nj];
+    const int bits = std::max(1, bit_length(static_cast<uint64_t>(max_n - 1)));
+    const int jbits = std::max(1, bit_length(static_cast<uint64_t>(nj - 1)));
+    if (2 * bits + jbits > 64 || max_n > (int64_t{1} << 31))
+      throw std::out_of_range("build_mask: frame pair too large for the sampling key");
+    const int64_t ncnt = assign_counts(P, batch);
+    P.d_jobs.upload(P.djobs.data(), P.djobs.size());
+    DevBuf<int> d_batch(nj, s);
+    d_batch.upload(batch.data(), nj);
+    DevBuf<int64_t> d_off(nj + 1, s);
+    d_off.upload(off.data(), nj + 1);
+    DevBuf<uint64_t> keys(total, s), sorted(total, s);
+    DevBuf<int32_t> prev(total, s), tlast(total, s);
+    DevBuf<uint32_t> counts(ncnt, s);
+    RP_CUDA(cudaMemsetAsync(tlast.p, 0xFF, sizeof(int32_t) * total, s));
+    RP_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(uint32_t) * ncnt, s));
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+    fy_draw_kernel<<<grid, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, nj, total, bits, keys.p);
+    RP_LAUNCHED();
+    size_t tmp_bytes = 0;
+    const int end_bit = 2 * bits + jbits;
+    RP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, total, 0,
+                                           end_bit, s));
+    DevBuf<uint8_t> tmp(tmp_bytes, s);
+    RP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, total, 0, end_bit,
+                                           s));
+    count_launch();
+    fy_link_kernel<<<grid, 256, 0, s>>>(sorted.p, total, bits, d_off.p, prev.p, tlast.p,
+                                        P.d_jobs.p, d_batch.p);
+    RP_LAUNCHED();
+    fy_count_kernel<<<grid, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, nj, total, prev.p,
+                                         tlast.p, counts.p, nt, bs);
+    RP_LAUNCHED();
+    std::vector<Item> items;
+    for (int jx : batch) tiles_of(P, jx, items);
+    launch_apply(P, items, counts.p, words, 1, s);
+    P.sampled += total;
+  }
+}
+
+Feat make_feat(const rp_tensor* q, const rp_tensor* k, int heads) {
+  Feat f;
+  f.q = q->data;
+  f.k = k->data;
+  f.dtype = q->dtype;
+  f.q_ts = q->token_stride;
+  f.q_hs = q->head_stride;
+  f.k_ts = k->token_stride;
+  f.k_hs = k->head_stride;
+  f.heads = heads;
+  f.d = q->head_dim;
+  f.inv_sqrt_d = 1.0 / std::sqrt(static_cast<double>(q->head_dim));
+  return f;
+}
+
+void build_dynamic_exact(rp_plan_s& P, const Feat& f, uint32_t* words, int64_t* rechecked,
+                         int64_t* fallbacks, cudaStream_t s) {
+  const int bs = P.g.block_size;
+  const int64_t nt = P.g.tokens_per_frame;
+  auto bl = batches(P, plan::kScore, kScoreCap, [](const DJob& d) { return d.n; });
+  (void)rechecked;
+  for (auto& batch : bl) {
+    const int nj = static_cast<int>(batch.size());
+    std::vector<int64_t> off(nj + 1, 0);
+    for (int x = 0; x < nj; ++x) off[x + 1] = off[x] + P.djobs[batch[x]].n;
+    const int64_t total = off[nj];
+    const int64_t ncnt = assign_counts(P, batch);
+    P.d_jobs.upload(P.djobs.data(), P.djobs.size());
+    DevBuf<int> d_batch(nj, s);
+    d_batch.upload(batch.data(), nj);
+    DevBuf<int64_t> d_off(nj + 1, s);
+    d_off.upload(off.data(), nj + 1);
+    DevBuf<float> scores(total, s);
+    DevBuf<double2> stats(nj, s);
+    DevBuf<uint32_t> counts(ncnt, s);
+    DevBuf<unsigned long long> kept(nj + 1, s);
+    RP_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(uint32_t) * ncnt, s));
+    RP_CUDA(cudaMemsetAsync(kept.p, 0, sizeof(unsigned long long) * (nj + 1), s));
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+    exact_scores_kernel<<<grid, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, nj, total, f, nt,
+                                             scores.p);
+    RP_LAUNCHED();
+    seq_stats_kernel<<<(nj + 63) / 64, 64, 0, s>>>(d_off.p, nj, scores.p, stats.p);
+    RP_LAUNCHED();
+    exact_select_kernel<<<grid, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, nj, total,
+                                             scores.p, stats.p, counts.p, kept.p, nt, bs);
+    RP_LAUNCHED();
+    exact_fallback_kernel<<<nj, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, scores.p, stats.p,
+                                             kept.p, counts.p, nt, bs, P.c.fallback_k,
+                                             kept.p + nj);
+    RP_LAUNCHED();
+    std::vector<Item> items;
+    for (int jx : batch) tiles_of(P, jx, items);
+    launch_apply(P, items, counts.p, words, 1, s);
+    if (fallbacks) {
+      unsigned long long h = 0;
+      RP_CUDA(cudaMemcpyAsync(&h, kept.p + nj, sizeof(h), cudaMemcpyDeviceToHost, s));
+      RP_CUDA(cudaStreamSynchronize(s));
+      *fallbacks += static_cast<int64_t>(h);
+    }
+    P.scored += total;
+  }
+}
+
+}  // namespace
+
 extern "C" {
+
 void rp_build_options_defaults(rp_build_options* o) {
   o->disable_split = 0;
   o->score_engine = 0;
   o->recheck_delta = 0.0;
 }
+
 rp_status rp_plan_create(const rp_grid* g, const rp_config* c, uint64_t seed,
                          const rp_build_options* opt, rp_plan* out) {
   return guarded([&] {
     check_grid(g);
+    if (!c) throw std::invalid_argument("config: null");
     plan::validate(*c);
-    auto* p = new rp_plan_s{*g, *c, seed, {}};
-    if (opt) p->o = *opt; else rp_build_options_defaults(&p->o);
-    *out = p;
+    std::unique_ptr<rp_plan_s> p(new rp_plan_s);
+    p->g = *g;
+    p->c = *c;
+    p->seed = seed;
+    if (opt) p->o = *opt;
+    else rp_build_options_defaults(&p->o);
+    make_jobs(*p);
+    p->words = static_cast<size_t>((g->blocks_per_dim * g->row_bytes + 3) / 4);
+    *out = p.release();
   });
 }
-void rp_plan_destroy(rp_plan p) { delete p; }
-rp_status rp_plan_build_mask(rp_plan, const rp_tensor*, const rp_tensor*, int, uint8_t*,
-                             rp_build_stats*, rp_stream) {
-  return guarded([&] { throw std::runtime_error("rp_plan_build_mask: not implemented yet"); });
+
+void rp_plan_destroy(rp_plan p) {
+  if (!p) return;
+  if (p->s) cudaStreamSynchronize(p->s);
+  delete p;
 }
+
+rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
+                             int n_score_heads, uint8_t* mask_bits_dev, rp_build_stats* stats,
+                             rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (!P) throw std::invalid_argument("build_mask: null plan");
+    if (!mask_bits_dev) throw std::invalid_argument("build_mask: null mask buffer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const rp_grid& g = P->g;
+    const bool dynamic = P->c.mode == RP_DYNAMIC_THRESHOLD;
+    if (dynamic) {
+      if (!q || !k || !q->data || !k->data)
+        throw std::invalid_argument("build_mask: dynamic mode needs features");
+      if (n_score_heads < 1 || n_score_heads > q->heads || q->heads != k->heads ||
+          q->head_dim != k->head_dim || q->dtype != k->dtype || q->head_dim < 1)
+        throw std::invalid_argument("feature batch: queries/keys shape mismatch");
+      if (q->tokens < g.total_tokens || k->tokens < g.total_tokens)
+        throw std::invalid_argument("build_mask: feature batch too short");
+    }
+    if (!P->d_jobs.p) {
+      P->s = s;
+      P->d_jobs = DevBuf<DJob>(std::max<size_t>(P->djobs.size(), 1), s, true);
+      if (!P->djobs.empty()) P->d_jobs.upload(P->djobs.data(), P->djobs.size());
+    }
+    if (!P->base_ready) build_base(*P, s);
+    const size_t bytes = static_cast<size_t>(g.blocks_per_dim * g.row_bytes);
+    int64_t rechecked = 0, fallbacks = 0;
+    if (!dynamic) {
+      if (!P->static_ready) {
+        P->cached = DevBuf<uint32_t>(P->words, s, true);
+        RP_CUDA(cudaMemcpyAsync(P->cached.p, P->base.p, P->words * 4, cudaMemcpyDeviceToDevice, s));
+        build_static(*P, P->cached.p, s);
+        P->static_ready = true;
+      }
+      RP_CUDA(cudaMemcpyAsync(mask_bits_dev, P->cached.p, bytes, cudaMemcpyDeviceToDevice, s));
+    } else {
+      DevBuf<uint32_t> work(P->words, s);
+      RP_CUDA(cudaMemcpyAsync(work.p, P->base.p, P->words * 4, cudaMemcpyDeviceToDevice, s));
+      const Feat f = make_feat(q, k, n_score_heads);
+      int engine = P->o.score_engine;
+      if (engine == 0)
+        engine = (q->dtype == RP_BF16 && fast_engine_supported(g, q->head_dim, n_score_heads))
+                     ? 1 : 2;
+      if (engine == 1) {
+        if (q->dtype != RP_BF16 || !fast_engine_supported(g, q->head_dim, n_score_heads))
+          throw std::invalid_argument(
+              "build_mask: tensor-core scoring needs bf16 features, B in {32,64,128} and "
+              "head_dim*heads in {64..512, multiple of 64}");
+        FastArgs a{q, k, n_score_heads, P->djobs, P->d_jobs.p, g, P->cmin, P->amin,
+                   P->c.fallback_k, P->o.recheck_delta > 0 ? P->o.recheck_delta : 1e-4,
+                   work.p, s, &rechecked, &fallbacks, stats != nullptr};
+        for (const DJob& d : P->djobs)
+          if (d.kind == plan::kScore) P->scored += d.n;
+        build_dynamic_fast(a, f);
+      } else {
+        build_dynamic_exact(*P, f, work.p, &rechecked, stats ? &fallbacks : nullptr, s);
+      }
+      RP_CUDA(cudaMemcpyAsync(mask_bits_dev, work.p, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    if (stats) {
+      std::vector<uint8_t> h(bytes);
+      RP_CUDA(cudaMemcpyAsync(h.data(), mask_bits_dev, bytes, cudaMemcpyDeviceToHost, s));
+      RP_CUDA(cudaStreamSynchronize(s));
+      int64_t act = 0;
+      for (uint8_t b : h) act += __builtin_popcount(b);
+      stats->retained_frame_pairs = P->retained;
+      stats->scored_pairs = P->scored;
+      stats->sampled_pairs = P->sampled;
+      stats->rechecked_pairs = rechecked;
+      stats->fallback_frame_pairs = fallbacks;
+      stats->active_blocks = act;
+    }
+  });
+}
+
 rp_status rp_build_mask(const rp_grid* g, const rp_config* c, uint64_t seed,
                         const rp_build_options* opt, const rp_tensor* q, const rp_tensor* k,
                         int n, uint8_t* bits, rp_build_stats* st, rp_stream s) {
@@ -39,7 +800,15 @@ rp_status rp_build_mask(const rp_grid* g, const rp_config* c, uint64_t seed,
   rp_status r = rp_plan_create(g, c, seed, opt, &p);
   if (r != RP_OK) return r;
   r = rp_plan_build_mask(p, q, k, n, bits, st, s);
+  if (r == RP_OK) {
+    const cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(s));
+    if (e != cudaSuccess) {
+      set_error(cudaGetErrorString(e));
+      r = RP_CUDA_ERROR;
+    }
+  }
   rp_plan_destroy(p);
   return r;
 }
-}
+
+}  // extern "C"

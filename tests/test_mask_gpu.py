@@ -1,0 +1,100 @@
+"""Stages (a)-(c) parity on the B200: device build_mask vs the reference.
+
+Bit-exact (integer/byte work): every golden mask of the compiled reference,
+the Wan2.1 config-3 production mask, and a sweep of random configs checked
+against the C restatement (itself pinned to the reference in test_oracle).
+"""
+import numpy as np
+import pytest
+import torch
+
+from golden_util import GOLDEN, case_id, features, mask_cases, read_drbm
+from oracle import pyoracle
+from oracle.pyoracle import Cfg
+from paper_2604_20470_b200 import radialplan as rp
+
+pytestmark = pytest.mark.gpu
+CASES = mask_cases()
+
+
+def to_cfg(c: Cfg) -> rp.SparsityConfig:
+    return rp.SparsityConfig(rp.Mode(c.mode),
+                             rp.RadialParams(c.decay_factor, c.long_range_factor,
+                                             c.split_epsilon),
+                             c.mask_threshold, c.col_threshold, c.near_param, c.far_param,
+                             c.fallback_k)
+
+
+def gpu_mask(nf, nt, bs, c, seed, disable_split=False, q=None, k=None, dtype=torch.float32,
+             engine=0, stats=None):
+    g = rp.make_grid(nf, nt, bs)
+    feats = None
+    if q is not None:
+        feats = rp.FeatureBatch(torch.from_numpy(q).cuda().to(dtype),
+                                torch.from_numpy(k).cuda().to(dtype))
+    m = rp.build_mask(g, to_cfg(c), seed, rp.BuildOptions(disable_split, engine), feats,
+                      stats=stats)
+    return m.bits
+
+
+@pytest.mark.parametrize("case", CASES, ids=[case_id(c) for c in CASES])
+def test_golden_masks_bit_exact(cuda, port, case):
+    q, k = features(port, case["features"])
+    got = gpu_mask(case["nf"], case["nt"], case["bs"], case["cfg"], case["seed"],
+                   case["disable_split"], q, k)
+    assert np.array_equal(got, case["bits"]), int((got != case["bits"]).sum())
+
+
+def test_wan_config3_static_bit_exact(cuda):
+    _, want = read_drbm(f"{GOLDEN}/wan_cfg3.drbm")
+    st = {}
+    got = gpu_mask(21, 3600, 128, Cfg(0, 1.0, 0.1, 1e-6, 1.0, 0.2, 0.3, 0.3), 7, stats=st)
+    assert np.array_equal(got, want)
+    assert st["active_blocks"] == 67743
+    assert st["sampled_pairs"] > 2e8  # 231.4M Fisher-Yates draws
+
+
+@pytest.mark.parametrize("bs", [4, 8, 16, 32, 64, 128])
+def test_static_random_configs_vs_oracle(cuda, port, bs):
+    rng = np.random.default_rng(bs)
+    for trial in range(6):
+        nf = int(rng.integers(2, 9))
+        nt = int(rng.integers(bs // 2 + 1, 3 * bs + 40))
+        c = Cfg(0, rng.uniform(1.0, 3.0), rng.uniform(0.1, 1.0), 1e-6, rng.uniform(0.1, 1.0),
+                rng.uniform(0.1, 1.0), rng.uniform(0.3, 1.0), rng.uniform(0.1, 0.8))
+        seed = int(rng.integers(0, 2**62))
+        want = port.build_mask(nf, nt, bs, c, seed, threads=4)
+        got = gpu_mask(nf, nt, bs, c, seed)
+        assert np.array_equal(got, want), (nf, nt, c, seed)
+
+
+def test_spec_criterion1_sweep_gpu(cuda, port):
+    """SPEC.md:783 sweep (B=4) through the GPU builder, both modes, exact engine."""
+    from test_oracle import spec_sweep
+    for mode in (0, 1):
+        for n, (nf, nt, c, seed, fs) in enumerate(spec_sweep(mode)):
+            if n % 5:  # every 5th case keeps the GPU suite short
+                continue
+            q = k = None
+            if mode == 1:
+                q, k = features(port, fs)
+            want = port.build_mask(nf, nt, 4, c, seed, False, q, k)
+            got = gpu_mask(nf, nt, 4, c, seed, False, q, k)
+            assert np.array_equal(got, want), (mode, nf, nt, c, seed)
+
+
+def test_static_mask_is_cached_per_plan(cuda):
+    g = rp.make_grid(8, 256, 32)
+    plan = rp.Plan(g, to_cfg(Cfg(0, 2.0, 0.3, 1e-6, 0.75, 0.2, 0.2, 0.2)), 7)
+    a = plan.build_mask_device().clone()
+    n0 = rp.kernel_launch_count()
+    b = plan.build_mask_device()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert rp.kernel_launch_count() == n0  # second call re-emits the cache
+
+
+def test_dynamic_needs_features(cuda):
+    g = rp.make_grid(4, 16, 4)
+    with pytest.raises(rp.InvalidArgument, match="dynamic mode needs features"):
+        rp.build_mask(g, rp.SparsityConfig(rp.Mode.DynamicThreshold), 1)

@@ -1,0 +1,99 @@
+"""CPU: pin the oracle (C restatement) against the reference's own outputs.
+
+* every golden mask (made by the compiled reference, tests/golden) is
+  reproduced bit for bit by the restatement;
+* SPEC acceptance criterion 1 run against the compiled
+  reference: N_f in 2..6, N_t in {4, 8, 12}, B = 4, 50 random Table-5 configs
+  per mode (1500 builds);
+* stage (d) restatement vs the reference's masked_attention_exact golden.
+"""
+import numpy as np
+import pytest
+
+from golden_util import GOLDEN, case_id, features, mask_cases, read_drbm
+from oracle import pyoracle
+from oracle.pyoracle import Cfg
+
+CASES = mask_cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[case_id(c) for c in CASES])
+def test_port_matches_golden_masks(port, case):
+    q, k = features(port, case["features"])
+    bits = port.build_mask(case["nf"], case["nt"], case["bs"], case["cfg"], case["seed"],
+                           case["disable_split"], q, k, threads=3)
+    assert np.array_equal(bits, case["bits"])
+
+
+def test_wan_config3_golden(port):
+    dim, bits = read_drbm(f"{GOLDEN}/wan_cfg3.drbm")
+    assert dim == 591
+    assert int(np.unpackbits(bits).sum()) == 67743  # sparsity 0.8061
+    got = port.build_mask(21, 3600, 128, Cfg(0, 1.0, 0.1, 1e-6, 1.0, 0.2, 0.3, 0.3), 7,
+                          threads=8)
+    assert np.array_equal(got, bits)
+
+
+def _spec_configs(mode, rng, n=50):
+    out = []
+    for _ in range(n):
+        g = rng.uniform(1.0, 3.0)
+        lam = rng.uniform(0.1, 1.0)
+        tc = rng.uniform(0.1, 1.0)
+        tm = rng.uniform(0.1, 1.0)
+        if mode == 0:
+            a, b = rng.uniform(0.3, 1.0), rng.uniform(0.1, 0.8)
+        else:
+            a, b = rng.uniform(-10.0, 5.0), rng.uniform(-5.0, 8.0)
+        out.append(Cfg(mode, g, lam, 1e-6, tm, tc, a, b, int(rng.integers(1, 4))))
+    return out
+
+
+def spec_sweep(mode, seed=2024):
+    rng = np.random.default_rng(seed + mode)
+    cfgs = _spec_configs(mode, rng)
+    for nf in range(2, 7):
+        for nt in (4, 8, 12):
+            for ci, c in enumerate(cfgs):
+                yield nf, nt, c, int(rng.integers(0, 2**63)), (nf * nt, 2, 8, 100 + ci)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_spec_criterion1_port_vs_reference(ref, port, mode):
+    n = 0
+    for nf, nt, c, seed, fs in spec_sweep(mode):
+        q = k = None
+        if mode == 1:
+            q, k = features(port, fs)
+        a = ref.build_mask(nf, nt, 4, c, seed, False, q, k)
+        b = port.build_mask(nf, nt, 4, c, seed, False, q, k)
+        assert np.array_equal(a, b), (nf, nt, c, seed)
+        n += 1
+    assert n == 750
+
+
+def test_random_batch_bit_identical(ref, port):
+    a = ref.random_batch(300, 3, 16, 42)
+    b = port.random_batch(300, 3, 16, 42, threads=3)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_attention_restatement_vs_reference_golden(port):
+    z = np.load(f"{GOLDEN}/attn_small.npz")
+    nf, nt, bs = int(z["nf"]), int(z["nt"]), int(z["bs"])
+    q, k, v = port.random_batch(nf * nt, 2, 32, int(z["seed"]), threads=2)
+    out = port.masked_attention_exact(nf, nt, bs, z["bits"], q, k, v, threads=4)
+    assert np.abs(out - z["exact"]).max() <= 1e-6
+    # soft vs exact differ by ~S'*eps mass: informational bound
+    assert np.abs(z["soft"] - z["exact"]).max() < 1e-6
+
+
+def test_static_select_stream_matches_reference(ref):
+    """static_select (selection.cpp:61-91): k = max(1, floor(n*rho)) distinct
+    pairs of the band, in shuffle order, from the pair's splitmix64 stream."""
+    c = Cfg(0, 2.0, 1.0)
+    uv = ref.static_select(8, 8, 4, c, 0, 2, 0.25, 99)
+    assert len(uv) == 13  # |P| = 52
+    assert len({tuple(x) for x in uv}) == 13
+    assert all(abs(u - v) <= 4 for u, v in uv)
