@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdynrad.so")
+LIB_PATH = os.environ.get("DYNRAD_LIB") or os.path.join(HERE, "libdynrad.so")
 
 
 # --- exceptions mirroring the reference's exception types -----------------

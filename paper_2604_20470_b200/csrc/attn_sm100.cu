@@ -9,16 +9,22 @@
 //     TMA's out-of-bounds fill produces them, and padded keys take part with
 //     logit 0 whenever their block is active (attention.cpp:43-48, 66-68).
 //
-// Design (one persistent CTA per SM, 320 threads, FA4-style warp roles):
+// Design (one persistent CTA per SM, 384 threads, FA4-style warp roles):
 //   warps 0-3  softmax for tile A  (thread t owns query row t = TMEM lane t)
 //   warps 4-7  softmax for tile B
 //   warp  8    TMA producer (Q tiles, K/V ring of kStages 128-row tiles)
 //   warp  9    TMEM allocator + tcgen05.mma issuer (one thread)
+//   warps 10-11 idle (complete the producer warpgroup for setmaxnreg)
 // A work unit is (row block r, head pair {2p, 2p+1}): tiles A and B share
-// the same KV block list, so while softmax(A) runs the tensor core computes
-// the other tile (ping-pong).  TMEM (512 cols): S_A 0-127, S_B 128-255,
-// O_A 256-(256+D), O_B 384-(384+D); P (bf16) overwrites S's first D/2...64
-// columns and feeds the P.V MMA straight from TMEM (A operand in TMEM).
+// the same KV block list and ping-pong on the tensor core.  TMEM (512 cols):
+// S_A 0-127, S_B 128-255, O_A 256-(256+D), O_B 384-(384+D).  P (bf16)
+// overwrites the first 64 columns of its S tile and feeds O += P V straight
+// from TMEM (A operand in TMEM), so shared memory only serves Q, K and V
+// (the tensor core's shared-memory read bandwidth is the scarce resource for
+// 1-SM 128x128 MMAs; a P operand in shared memory measured ~8% slower).
+// MMA issue order per step j: O_A += P_A(j) V(j), S_A(j+1), O_B += P_B(j)
+// V(j), S_B(j+1) (S_x(j+1) overwrites P_x(j), so it follows the P.V that
+// reads it; tcgen05 MMAs of one CTA execute in issue order).
 // Online softmax with lazy rescaling: O and l are rescaled only when the row
 // max grows by more than 2^8 (exact: numerator and denominator share the
 // stale max).
@@ -27,17 +33,24 @@
 namespace rp {
 namespace attn {
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;  // 3 warpgroups: softmax A, softmax B, producer/MMA
 constexpr int kBM = 128;  // query rows per tile (= block size B)
 constexpr int kBN = 128;  // keys per KV tile (= block size B)
+// Which of every 8 consecutive element pairs take the polynomial exp2 on the
+// FMA pipe instead of MUFU.EX2 (bit i set -> pair i mod 8 uses the
+// polynomial): balances the two pipes, FA4-style.
+#ifndef RP_POLY_MASK
+#define RP_POLY_MASK 0x00u
+#endif
+constexpr uint32_t kPolyMask = RP_POLY_MASK;
 
 template <int D>
 struct Layout {
   static constexpr int kChunks = D / 64;           // 128-byte K chunks
   static constexpr int kTileBytes = 128 * D * 2;   // one 128-row bf16 tile
   static constexpr int kChunkBytes = 128 * 128;    // 128 rows x 128 B
-  static constexpr int kStages = D == 128 ? 4 : 8;
-  static constexpr int kSmemData = (2 + kStages) * kTileBytes;
+  static constexpr int kStages = D == 128 ? 5 : 10;
+  static constexpr int kSmemData = 2 * kTileBytes + kStages * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 12;
   static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + 1024;
   RP_HD static uint32_t s_col(int x) { return x ? 128u : 0u; }
@@ -85,17 +98,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sq = smem;                            // [2][tile]
-  uint8_t* skv = smem + 2 * L::kTileBytes;       // [kStages][tile]
+  uint8_t* sq = smem;                                  // [2][tile]
+  uint8_t* skv = smem + 2 * L::kTileBytes;             // [kStages][tile]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kSmemData);
   uint64_t* kv_full = bars;
   uint64_t* kv_empty = bars + L::kStages;
-  uint64_t* q_full = bars + 2 * L::kStages;      // [2]
+  uint64_t* q_full = bars + 2 * L::kStages;  // [2] each below
   uint64_t* q_empty = q_full + 2;
-  uint64_t* s_full = q_full + 4;
-  uint64_t* p_full = q_full + 6;
-  uint64_t* o_done = q_full + 8;
-  uint64_t* o_free = q_full + 10;
+  uint64_t* s_full = q_full + 4;    // MMA -> softmax: S_x ready in TMEM
+  uint64_t* p_full = q_full + 6;    // softmax -> MMA: P_x written to TMEM
+  uint64_t* o_done = q_full + 8;    // MMA -> softmax: unit's last P.V done
+  uint64_t* o_free = q_full + 10;   // softmax -> MMA: epilogue read O_x
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
 
   const int warp = threadIdx.x / 32;
@@ -127,11 +140,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
-    // ------------------------------------------------------ TMA producer --
-    if (lane == 0) {
+  // Register budget per role: the launch allocates 168 regs x 384 threads;
+  // the producer warpgroup gives back to 88 so the two softmax warpgroups
+  // (128-wide score row + packed P) can grow to 208:
+  // 2 * 128 * 208 + 128 * 88 == 384 * 168 (an over-ask would block forever).
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    if (warp == 8 && lane == 0) {
+      // ---------------------------------------------------- TMA producer --
       const uint64_t pol_q = policy_evict_first();
+#ifdef RP_KV_EVICT_NORMAL
+      const uint64_t pol_kv = policy_evict_normal();
+#else
       const uint64_t pol_kv = policy_evict_last();
+#endif
       uint32_t kv_it = 0;
       uint32_t ucnt[2] = {0, 0};
       auto load_kv = [&](const CUtensorMap* m, int h, int blk) {
@@ -142,8 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* dst = skv + st * L::kTileBytes;
 #pragma unroll
         for (int c = 0; c < L::kChunks; ++c)
-          tma_load_3d(dst + c * L::kChunkBytes, m, &kv_full[st], c * 64, h,
-                      blk * kBN, pol_kv);
+          tma_load_3d(dst + c * L::kChunkBytes, m, &kv_full[st], c * 64, h, blk * kBN, pol_kv);
         ++kv_it;
       };
       for (long long u = blockIdx.x; u < p.n_units; u += gridDim.x) {
@@ -154,10 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&q_full[x], L::kTileBytes);
 #pragma unroll
           for (int c = 0; c < L::kChunks; ++c)
-            tma_load_3d(sq + x * L::kTileBytes + c * L::kChunkBytes, &tq,
-                        &q_full[x], c * 64, x ? w.h1 : w.h0, w.row * kBM, pol_q);
+            tma_load_3d(sq + x * L::kTileBytes + c * L::kChunkBytes, &tq, &q_full[x], c * 64,
+                        x ? w.h1 : w.h0, w.row * kBM, pol_q);
           ++ucnt[x];
         }
+        // order must match the MMA issue order below
         const int32_t* cols = p.col_idx + w.beg;
         int cj = __ldg(cols);
         load_kv(&tk, w.h0, cj);
@@ -173,10 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           cj = cn;
         }
       }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------- MMA issuer ---
-    if (lane == 0) {
+    } else if (warp == 9 && lane == 0) {
+      // ----------------------------------------------------- MMA issuer ---
       const uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
       const uint32_t idesc_pv = idesc_bf16(128, D, false, true);
       const uint32_t sq_addr = smem_u32(sq);
@@ -202,18 +222,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (last_s) umma_commit(&q_empty[x]);
         ++kv_it;
       };
-      // O_x (+)= P_x . V : 128 x D, K = 128 keys in steps of 16; P in TMEM.
+      // O_x (+)= P_x . V : 128 x D, K = 128 keys in steps of 16; P in TMEM
+      // (bf16 pairs packed in the S_x columns 0..63).
       auto issue_pv = [&](int x, bool first, bool last) {
         const uint32_t st = kv_it % L::kStages;
         mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
         tc_fence_after();
         const uint32_t vb = skv_addr + st * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
+        for (int kk = 0; kk < kBN / 16; ++kk)
           umma_ts(tmem + L::o_col(x), tmem + L::s_col(x) + kk * 8,
-                  smem_desc_sw128(vb + kk * 16 * 128, L::kChunkBytes, 1024),
-                  idesc_pv, (!first) || kk > 0);
-        }
+                  smem_desc_sw128(vb + kk * 16 * 128, L::kChunkBytes, 1024), idesc_pv,
+                  (!first) || kk > 0);
         umma_commit(&kv_empty[st]);
         if (last) umma_commit(&o_done[x]);
         ++kv_it;
@@ -239,10 +259,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     // --------------------------------------------------------- softmax ----
     const int x = warp / 4;  // tile
     const int wq = warp % 4; // TMEM lane quarter
-    const int row_in_tile = wq * 32 + lane;
+    const int r = wq * 32 + lane;  // row within the tile
     const uint32_t trow = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const float sl2 = p.scale_log2;
     uint32_t scnt = 0, ucnt = 0;
@@ -255,67 +276,101 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&s_full[x], scnt & 1);
         ++scnt;
         tc_fence_after();
-        uint32_t s[128];
-        tmem_ld32(trow + L::s_col(x) + 0, *reinterpret_cast<uint32_t(*)[32]>(s + 0));
-        tmem_ld32(trow + L::s_col(x) + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
-        tmem_ld32(trow + L::s_col(x) + 64, *reinterpret_cast<uint32_t(*)[32]>(s + 64));
-        tmem_ld32(trow + L::s_col(x) + 96, *reinterpret_cast<uint32_t(*)[32]>(s + 96));
+        uint32_t s0[32], s1[32], s2[32], s3[32];
+        tmem_ld32(trow + L::s_col(x) + 0, s0);
+        tmem_ld32(trow + L::s_col(x) + 32, s1);
+        tmem_ld32(trow + L::s_col(x) + 64, s2);
+        tmem_ld32(trow + L::s_col(x) + 96, s3);
         tmem_wait_ld();
-        float mx = __uint_as_float(s[0]);
+        auto S = [&](int e) -> float {
+          const uint32_t v = e < 32 ? s0[e] : e < 64 ? s1[e - 32] : e < 96 ? s2[e - 64] : s3[e - 96];
+          return __uint_as_float(v);
+        };
+        // row max: four independent 3-input-max chains
+        float mq[4];
 #pragma unroll
-        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(s[i]));
+        for (int c = 0; c < 4; ++c) {
+          float a = S(32 * c);
+#pragma unroll
+          for (int i = 1; i < 31; i += 2) a = fmaxf(a, fmaxf(S(32 * c + i), S(32 * c + i + 1)));
+          mq[c] = fmaxf(a, S(32 * c + 31));
+        }
+        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         const float m_new = fmaxf(m, mx);
         bool need = false;
+        float alpha = 1.0f;
         if (j == 0) {
           m = m_new;
-        } else {
-          need = (m_new - m) * sl2 > 8.0f;
+        } else if ((m_new - m) * sl2 > 8.0f) {
+          need = true;
+          alpha = ex2((m - m_new) * sl2);
+          m = m_new;
+          l *= alpha;
         }
-        if (__any_sync(0xFFFFFFFFu, need)) {
-          const float alpha = need ? ex2((m - m_new) * sl2) : 1.0f;
-          if (need) {
-            m = m_new;
-            l *= alpha;
+        // p = 2^(s*scale*log2e - m*scale*log2e).  Two phases so the 128
+        // exponentials (MUFU and polynomial) issue back to back, independent
+        // of each other, before any consumer touches a result: the sums and
+        // bf16 packing then run on completed values instead of stalling on
+        // MUFU latency pair by pair.
+        const float2 sc2 = make_float2(sl2, sl2);
+        const float2 ng2 = make_float2(-m * sl2, -m * sl2);
+        auto put = [&](int e, float v) {
+          const uint32_t b = __float_as_uint(v);
+          if (e < 32) s0[e] = b; else if (e < 64) s1[e - 32] = b;
+          else if (e < 96) s2[e - 64] = b; else s3[e - 96] = b;
+        };
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float2 xv = ffma2(make_float2(S(2 * i), S(2 * i + 1)), sc2, ng2);
+          float2 pv;
+          if (kPolyMask & (1u << (i & 7))) {
+            pv = ex2_poly2(xv);
+          } else {
+            pv.x = ex2(xv.x);
+            pv.y = ex2(xv.y);
           }
+          put(2 * i, pv.x);
+          put(2 * i + 1, pv.y);
+        }
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        uint32_t pk[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float2 pv = make_float2(S(2 * i), S(2 * i + 1));
+          acc[i & 3] = fadd2(acc[i & 3], pv);
+          pk[i] = pack_bf16(pv.x, pv.y);
+        }
+        const float2 at = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        l += at.x + at.y;
+        // (O_x is stable here: S_x(j) was issued after O_x += P_x(j-1) V(j-1)
+        // and its commit covers every earlier MMA.)
+        if (__any_sync(0xFFFFFFFFu, need)) {
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
             tmem_ld32(trow + L::o_col(x) + c * 32, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
             tmem_st32(trow + L::o_col(x) + c * 32, o);
           }
-          tmem_wait_st();
         }
-        const float neg = -m * sl2;
-        float sum = 0.f;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          uint32_t pk[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float p0 = ex2(fmaf(__uint_as_float(s[half * 64 + 2 * i]), sl2, neg));
-            const float p1 = ex2(fmaf(__uint_as_float(s[half * 64 + 2 * i + 1]), sl2, neg));
-            sum += p0 + p1;
-            pk[i] = pack_bf16(p0, p1);
-          }
-          tmem_st32(trow + L::s_col(x) + half * 32, pk);
-        }
-        l += sum;
+        // P row -> TMEM columns 0..63 of S_x (bf16 pairs, A operand of P.V)
+        tmem_st32(trow + L::s_col(x), *reinterpret_cast<const uint32_t(*)[32]>(pk));
+        tmem_st32(trow + L::s_col(x) + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[x]);
       }
-      // epilogue: O / l -> bf16 -> global
+      // epilogue: wait for the unit's last P.V, O / l -> bf16 -> global
       mbar_wait(&o_done[x], ucnt & 1);
       ++ucnt;
       tc_fence_after();
       const float inv = 1.0f / l;
       const int h = x ? w.h1 : w.h0;
-      const long long tok = static_cast<long long>(w.row) * kBM + row_in_tile;
+      const long long tok = static_cast<long long>(w.row) * kBM + r;
       __nv_bfloat16* orow = p.out + tok * p.out_tok_stride + h * p.out_head_stride;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {

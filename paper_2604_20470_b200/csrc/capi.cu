@@ -110,10 +110,19 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     p.out_head_stride = o.head_stride;
     p.scale_log2 = scale * 1.4426950408889634f;
     const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
+    // The kernel re-balances registers between warpgroups with setmaxnreg;
+    // that only works if the launch allocates the full 168 x 384 pool.
+    auto check_regs = [](const void* fn) {
+      cudaFuncAttributes fa;
+      RP_CUDA(cudaFuncGetAttributes(&fa, fn));
+      if (fa.numRegs * attn::kThreads < 2 * 128 * 208 + 128 * 88)
+        throw CudaError("bsfa_fwd_kernel compiled with too few registers for its setmaxnreg plan");
+    };
     if (d == 128) {
       static bool attr = false;
       const int smem = attn::Layout<128>::kSmemBytes;
       if (!attr) {
+        check_regs(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<128>));
         RP_CUDA(cudaFuncSetAttribute(attn::bsfa_fwd_kernel<128>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
@@ -123,6 +132,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       static bool attr = false;
       const int smem = attn::Layout<64>::kSmemBytes;
       if (!attr) {
+        check_regs(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<64>));
         RP_CUDA(cudaFuncSetAttribute(attn::bsfa_fwd_kernel<64>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
