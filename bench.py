@@ -221,10 +221,8 @@ def main():
 
     peaks, peaks_kind = load_peaks()
     H, d = cfgd["heads"], cfgd["d"]
-    # contiguous head shard per rank
-    per = [H // world + (1 if r < H % world else 0) for r in range(world)]
-    h0 = sum(per[:rank])
-    Hl = per[rank]
+    from paper_2604_20470_b200.sharding import broadcast_mask, head_shards
+    h0, Hl = head_shards(H, world)[rank]  # contiguous head shard per rank
     g = rp.make_grid(cfgd["nf"], cfgd["nt"], cfgd["bs"])
     gm, gl, tm, tc, a, b = cfgd["cfg"]
     cfg = rp.SparsityConfig(rp.Mode(cfgd["mode"]), rp.RadialParams(gm, gl), tm, tc, a, b)
@@ -248,6 +246,8 @@ def main():
         e0.record(stream)
         mask = plan.build_mask_device(q if dynamic else None, k if dynamic else None,
                                       2 if dynamic else 0, stream=stream)
+        if dynamic and world > 1:
+            broadcast_mask(mask, src=0)
         row_ptr, col_idx, order = rp.mask_to_csr(g, mask, stream=stream)
         e1.record(stream)
     stream.synchronize()
@@ -256,10 +256,23 @@ def main():
     nb = g.blocks_per_dim
     sparsity = 1.0 - nnz / float(nb * nb)
 
+    csr_bufs = None
+    if dynamic:
+        csr_bufs = (torch.empty(nb + 1, dtype=torch.int32, device=dev),
+                    torch.empty(nb * nb, dtype=torch.int32, device=dev),
+                    torch.empty(nb, dtype=torch.int32, device=dev),
+                    torch.zeros(1, dtype=torch.int64, device=dev))
+
     def layer():
+        nonlocal row_ptr, col_idx, order
         if dynamic:
-            plan.build_mask_device(q, k, 2, out=mask, stream=stream)
-            rp.mask_to_csr(g, mask, stream=stream)
+            # the scoring heads (global 0..H_f-1) live on rank 0; it builds the
+            # mask and broadcasts the bitmask (one small NCCL collective)
+            if rank == 0:
+                plan.build_mask_device(q, k, 2, out=mask, stream=stream)
+            if world > 1:
+                broadcast_mask(mask, src=0)
+            row_ptr, col_idx, order = rp.mask_to_csr(g, mask, stream=stream, out=csr_bufs)
         rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, out=out, stream=stream)
 
     with torch.cuda.stream(stream):

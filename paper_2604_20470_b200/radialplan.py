@@ -438,21 +438,31 @@ def build_mask(g: GridSpec, c: SparsityConfig, seed: int,
     return BlockMask(g.blocks_per_dim, dev.cpu().numpy())
 
 
-def mask_to_csr(g: GridSpec, mask_dev, stream=None):
-    """Bit-packed device mask -> (row_ptr[S_b+1], col_idx[nnz], row_order[S_b]) int32."""
+def mask_to_csr(g: GridSpec, mask_dev, stream=None, out=None, trim: bool = True):
+    """Bit-packed device mask -> (row_ptr[S_b+1], col_idx, row_order[S_b]) int32.
+
+    With trim=False (or preallocated `out` buffers) nothing synchronizes:
+    col_idx keeps its S_b^2 capacity and only row_ptr delimits the lists,
+    which is what the per-layer dynamic path uses."""
     torch = _torch()
     nb = g.blocks_per_dim
-    row_ptr = torch.empty(nb + 1, dtype=torch.int32, device="cuda")
     cap = nb * nb
-    col_idx = torch.empty(cap, dtype=torch.int32, device="cuda")
-    order = torch.empty(nb, dtype=torch.int32, device="cuda")
-    nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if out is None:
+        row_ptr = torch.empty(nb + 1, dtype=torch.int32, device="cuda")
+        col_idx = torch.empty(cap, dtype=torch.int32, device="cuda")
+        order = torch.empty(nb, dtype=torch.int32, device="cuda")
+        nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+    else:
+        row_ptr, col_idx, order, nnz = out
+        cap = col_idx.numel()
     gc = g.c()
     L.check(L.lib().rp_mask_to_csr(C.byref(gc), C.c_void_p(mask_dev.data_ptr()),
                                    C.c_void_p(row_ptr.data_ptr()),
                                    C.c_void_p(col_idx.data_ptr()), cap,
                                    C.c_void_p(order.data_ptr()), C.c_void_p(nnz.data_ptr()),
                                    _stream(stream)))
+    if not trim or out is not None:
+        return row_ptr, col_idx, order
     n = int(nnz.item())
     return row_ptr, col_idx[:n], order
 
