@@ -29,38 +29,11 @@
 #include "common.cuh"
 #include "internal.hpp"
 #include "mask_build.cuh"
+#include "mask_common.cuh"
 #include "plan.hpp"
 
 namespace rp {
 namespace mask {
-
-// ------------------------------------------------------------ helpers -----
-RP_DEV void set_block(uint32_t* words, int64_t row_bytes, int64_t r, int64_t c) {
-  const int64_t byte = r * row_bytes + c / 8;
-  atomicOr(&words[byte >> 2], 1u << (((byte & 3) << 3) + (c & 7)));
-}
-
-// Offsets of the canonical row-major band enumeration (radial.cpp:64-79) in
-// closed form: off(u) = sum_{x<u} (min(N-1, x+w) - max(0, x-w) + 1).
-RP_HD int64_t band_off(int64_t u, int64_t N, int64_t w) {
-  int64_t a = N - w;
-  if (a < 0) a = 0;
-  if (a > u) a = u;
-  const int64_t hi = a * (a - 1) / 2 + a * w + (u - a) * (N - 1);
-  int64_t c = u - 1 - w;
-  if (c < 0) c = 0;
-  return hi - c * (c + 1) / 2 + u;
-}
-// Flat index -> (u, v): largest u with off(u) <= flat (upper_bound - 1).
-RP_HD void band_uv(int64_t flat, int64_t N, int64_t w, int64_t* u, int64_t* v) {
-  int64_t lo = 0, hi = N;  // off(lo) <= flat < off(hi)
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (band_off(mid, N, w) <= flat) lo = mid; else hi = mid;
-  }
-  *u = lo;
-  *v = (lo - w > 0 ? lo - w : 0) + (flat - band_off(lo, N, w));
-}
 
 // ---------------------------------------------------- K1: base mask -------
 __global__ void intra_kernel(uint32_t* words, int nf, int64_t nt, int bs, int64_t row_bytes,
@@ -72,60 +45,6 @@ __global__ void intra_kernel(uint32_t* words, int nf, int64_t nt, int bs, int64_
     const int64_t r = b0 + x / span, c = b0 + x % span;
     if (r <= b1 && c <= b1) set_block(words, row_bytes, r, c);
   }
-}
-
-// Per (job, tile) item with B (<= 1024) threads: one column each.
-// mode 0: closed-form full-band counts; mode 1: counts from a buffer.
-__global__ void apply_kernel(const DJob* __restrict__ jobs, const Item* __restrict__ items,
-                             const uint32_t* __restrict__ counts, uint32_t* words, int64_t nt,
-                             int bs, int64_t row_bytes, int cmin, int amin, int mode) {
-  const Item it = items[blockIdx.x];
-  const DJob& jb = jobs[it.job];
-  __shared__ int active;
-  if (threadIdx.x == 0) active = 0;
-  __syncthreads();
-  int mine = 0;
-  for (int k = threadIdx.x; k < bs; k += blockDim.x) {
-    uint32_t cnt = 0;
-    if (mode == 0) {
-      // mask.cpp:132-158: column v of frame j hit by rows [v-w, v+w] of frame i
-      const int64_t qi = static_cast<int64_t>(jb.i) * nt, kj = static_cast<int64_t>(jb.j) * nt;
-      const int64_t gc = (jb.c0 + it.tc) * bs + k;
-      const int64_t lv = gc - kj;
-      if (lv >= 0 && lv < nt) {
-        const int64_t ulo = lv - jb.width > 0 ? lv - jb.width : 0;
-        const int64_t uhi = lv + jb.width < nt - 1 ? lv + jb.width : nt - 1;
-        const int64_t R0 = (jb.r0 + it.tr) * bs, R1 = R0 + bs - 1;
-        const int64_t lo = qi + ulo > R0 ? qi + ulo : R0;
-        const int64_t hi = qi + uhi < R1 ? qi + uhi : R1;
-        if (ulo <= uhi && lo <= hi) cnt = static_cast<uint32_t>(hi - lo + 1);
-      }
-    } else {
-      cnt = counts[jb.cnt_off + (static_cast<int64_t>(it.tr) * jb.tc + it.tc) * bs + k];
-    }
-    mine += cnt >= static_cast<uint32_t>(cmin);
-  }
-  if (mine) atomicAdd(&active, mine);
-  __syncthreads();
-  if (threadIdx.x == 0 && active >= amin)
-    set_block(words, row_bytes, jb.r0 + it.tr, jb.c0 + it.tc);
-}
-
-RP_DEV void add_count(const DJob& jb, uint32_t* counts, int64_t nt, int bs, int64_t u,
-                      int64_t v) {
-  const int64_t gr = static_cast<int64_t>(jb.i) * nt + u;
-  const int64_t gc = static_cast<int64_t>(jb.j) * nt + v;
-  const int64_t rr = gr / bs - jb.r0, cc = gc / bs - jb.c0;
-  atomicAdd(&counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs], 1u);
-}
-
-RP_DEV int find_job(const int64_t* __restrict__ off, int n_jobs, int64_t x) {
-  int lo = 0, hi = n_jobs;  // off[lo] <= x < off[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (off[mid] <= x) lo = mid; else hi = mid;
-  }
-  return lo;
 }
 
 // ------------------------------------------ K4: exact partial Fisher-Yates --
@@ -202,35 +121,6 @@ __global__ void fy_count_kernel(const DJob* __restrict__ jobs, const int* __rest
 }
 
 // ------------------------------------ K2/K3 exact engine (fp64 SIMT) -------
-struct Feat {
-  const void* q;
-  const void* k;
-  int dtype;
-  int64_t q_ts, q_hs, k_ts, k_hs;
-  int heads, d;
-  double inv_sqrt_d;
-};
-
-RP_DEV float feat_at(const void* p, int dtype, int64_t idx) {
-  return dtype == RP_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[idx])
-                          : static_cast<const float*>(p)[idx];
-}
-
-// selection.cpp:104-121: per-head dot in double (ascending d), acc +=
-// dot * inv_sqrt_d (no contraction), float(acc / heads).
-RP_DEV float exact_score(const Feat& f, int64_t qrow, int64_t krow) {
-  double acc = 0.0;
-  for (int h = 0; h < f.heads; ++h) {
-    const int64_t qb = qrow * f.q_ts + h * f.q_hs, kb = krow * f.k_ts + h * f.k_hs;
-    double dot = 0.0;
-    for (int e = 0; e < f.d; ++e)
-      dot = __fma_rn(static_cast<double>(feat_at(f.q, f.dtype, qb + e)),
-                     static_cast<double>(feat_at(f.k, f.dtype, kb + e)), dot);
-    acc = __dadd_rn(acc, __dmul_rn(dot, f.inv_sqrt_d));
-  }
-  return __double2float_rn(__ddiv_rn(acc, static_cast<double>(f.heads)));
-}
-
 __global__ void exact_scores_kernel(const DJob* __restrict__ jobs,
                                     const int* __restrict__ batch_jobs,
                                     const int64_t* __restrict__ off, int n_jobs, int64_t total,
@@ -261,10 +151,6 @@ __global__ void seq_stats_kernel(const int64_t* __restrict__ off, int n_jobs,
     sq = __dadd_rn(sq, __dmul_rn(dd, dd));
   }
   stats[lj] = make_double2(mean, __dsqrt_rn(__ddiv_rn(sq, static_cast<double>(n))));
-}
-
-RP_DEV double zscore(float s, double2 st) {
-  return __ddiv_rn(__dsub_rn(static_cast<double>(s), st.x), __dadd_rn(st.y, 1e-8));
 }
 
 __global__ void exact_select_kernel(const DJob* __restrict__ jobs,
@@ -429,6 +315,9 @@ struct rp_plan_s {
   DevBuf<uint32_t> cached;  // static mode: the full mask
   bool base_ready = false, static_ready = false;
   int64_t retained = 0, sampled = 0, scored = 0;
+  FastEngine* fast = nullptr;
+  int fast_heads = 0, fast_dim = 0;
+  ~rp_plan_s() { fast_engine_destroy(fast); }
 };
 
 namespace {
@@ -766,12 +655,20 @@ rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
           throw std::invalid_argument(
               "build_mask: tensor-core scoring needs bf16 features, B in {32,64,128} and "
               "head_dim*heads in {64..512, multiple of 64}");
-        FastArgs a{q, k, n_score_heads, P->djobs, P->d_jobs.p, g, P->cmin, P->amin,
-                   P->c.fallback_k, P->o.recheck_delta > 0 ? P->o.recheck_delta : 1e-4,
-                   work.p, s, &rechecked, &fallbacks, stats != nullptr};
-        for (const DJob& d : P->djobs)
-          if (d.kind == plan::kScore) P->scored += d.n;
-        build_dynamic_fast(a, f);
+        if (!P->fast || P->fast_heads != n_score_heads || P->fast_dim != q->head_dim) {
+          fast_engine_destroy(P->fast);
+          P->fast = nullptr;
+          P->fast = fast_engine_create(g, P->djobs, P->cmin, P->amin, n_score_heads,
+                                       q->head_dim, s);
+          P->fast_heads = n_score_heads;
+          P->fast_dim = q->head_dim;
+        }
+        FastResult fr;
+        fast_engine_run(P->fast, q, k, f, work.p, s,
+                        P->o.recheck_delta > 0 ? P->o.recheck_delta : 1e-5, P->c.fallback_k,
+                        stats != nullptr, &fr);
+        rechecked = fr.rechecked;
+        fallbacks = fr.fallbacks;
       } else {
         build_dynamic_exact(*P, f, work.p, &rechecked, stats ? &fallbacks : nullptr, s);
       }

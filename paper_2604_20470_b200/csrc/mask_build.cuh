@@ -28,26 +28,26 @@ struct Item {  // one (job, tile) of a job's rectangle
   int32_t job, tr, tc;
 };
 
+
+
 struct Feat;
 
-struct FastArgs {
-  const rp_tensor* q;
-  const rp_tensor* k;
-  int heads;
-  const std::vector<DJob>& jobs;
-  const DJob* d_jobs;
-  const rp_grid& g;
-  int cmin, amin, fallback_k;
-  double delta;
-  uint32_t* words;
-  cudaStream_t s;
-  int64_t* rechecked;
-  int64_t* fallbacks;
-  bool want_stats;
+// Tensor-core scoring engine (mask_score_sm100.cu).  Created once per plan
+// (it caches the tile list and device buffers of the plan's scored pairs).
+class FastEngine;
+struct FastResult {
+  int64_t rechecked = 0;   // pairs re-scored exactly in fp64
+  int64_t fallbacks = 0;   // frame pairs that took the fallback_k rule
 };
-
 bool fast_engine_supported(const rp_grid& g, int head_dim, int heads);
-void build_dynamic_fast(const FastArgs& a, const Feat& f);
+FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& jobs, int cmin,
+                               int amin, int heads, int head_dim, cudaStream_t s);
+void fast_engine_destroy(FastEngine* e);
+// Adds the selected tiles of every scored frame pair to `words` (the padded
+// 32-bit view of the bit-packed mask).
+void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, const Feat& f,
+                     uint32_t* words, cudaStream_t s, double delta_floor, int fallback_k,
+                     bool want_stats, FastResult* res);
 
 }  // namespace mask
 }  // namespace rp

@@ -1,13 +1,721 @@
-// Tensor-core dynamic scoring engine (placeholder until the tcgen05 kernel lands).
+// K2/K3: dynamic-threshold proxy scoring on the tensor cores (sm_100a).
+//
+// Reference semantics (selection.cpp:93-185): per ordered frame pair (i, j)
+// every band pair (u, v), |u - v| <= w, gets s = mean_h(q_u . k_v)/sqrt(d)
+// over the H_f scoring heads; s is standardised by the pair's population
+// mean / std and kept iff z >= tau; kept pairs are counted per tile column
+// and aggregated by the theta_c / theta_m rule (mask.cpp:87-125).
+//
+// B200 mapping.  The band of a frame pair is covered by 128 x 128 token tiles
+// (items).  One tcgen05 MMA chain per item computes S = Q' K'^T with
+// Q' = [q_h0 | q_h1 | ...] (the first H_f heads are adjacent in the [S, H, d]
+// layout, so the concatenation is one TMA box per head and 64-wide chunk):
+// K = H_f * d.  Bf16 products are exact, so a fast score differs from the
+// reference's double-accumulated score only by the fp32 accumulation inside
+// the tensor core, bounded per pair by kappa * |q'_u| |k'_v| (Cauchy-Schwarz).
+//   pass 1 (stats): per item and row, two-pass (n, mean, M2) in registers,
+//          Chan-merged in double across rows; items are then merged per
+//          frame pair in a fixed order (deterministic mu / sigma).
+//   pass 2 (select): z = (s - mu)/(sigma + 1e-8); decided directly when
+//          |z - tau| exceeds the pair's error bound + delta_floor, otherwise
+//          queued; kept bits -> per-column counts by warp ballots -> the
+//          frame pair's [tile][B] count buffer.
+//   recheck: every queued pair is re-scored exactly as the reference does
+//          (fp64, sequential d, separate multiply / add, float cast).
+//   apply: theta_c / theta_m per tile (shared with the exact engine).
+// Frame pairs with no kept pair take the fallback_k rule on exact scores
+// (it can only change a tile when fallback_k >= ceil(theta_c * B)).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
 #include <stdexcept>
+#include <vector>
 
+#include "common.cuh"
+#include "internal.hpp"
 #include "mask_build.cuh"
+#include "mask_common.cuh"
+#include "plan.hpp"
+#include "tmap.hpp"
 
 namespace rp {
 namespace mask {
-bool fast_engine_supported(const rp_grid&, int, int) { return false; }
-void build_dynamic_fast(const FastArgs&, const Feat&) {
-  throw std::invalid_argument("build_mask: tensor-core scoring engine not available");
+
+struct ScoreItem {
+  int32_t job;  // index into the engine's job array
+  int32_t tr;   // 128-token tile row (global)
+  int32_t tc;   // 128-token tile column (global)
+  int32_t pad;
+};
+
+struct SParams {
+  const DJob* jobs;
+  const ScoreItem* items;
+  long long n_items;
+  int nt, bs, cph;       // tokens per frame, block size, 64-wide chunks per head
+  float score_scale;     // inv_sqrt_d / H_f
+  double* item_stats;    // pass 1: [n_items][3] (n, mean, M2)
+  const double2* job_stats;  // pass 2: mean, stddev per job
+  uint32_t* counts;
+  unsigned long long* job_kept;
+  int4* queue;
+  unsigned long long* queue_len;
+  long long queue_cap;
+  const float* qnorm;
+  const float* knorm;
+  float kappa;
+  float delta_floor;
+  Feat feat;  // exact re-score in place when the recheck queue is full
+};
+
+constexpr int kThreads = 192;  // warps 0-3 epilogue (row = thread), 4 TMA, 5 MMA
+constexpr int kChunkBytes = 128 * 128;
+
+template <int NC>
+struct SLayout {
+  static constexpr int kTileBytes = NC * kChunkBytes;
+  static constexpr int kStages = 2;
+  static constexpr int kSmemData = (1 + kStages) * kTileBytes;
+  static constexpr int kNumBars = 2 * kStages + 6;
+  // bars | tmem slot (16 B) | knorm[128] | wcnt[4][128] | red[4][3] doubles
+  static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 4 * 128 * 4 + 4 * 3 * 8;
+  static constexpr int kSmemBytes = kSmemData + kExtra + 1024;
+};
+
+RP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+struct Welford {
+  double n, mean, m2;
+};
+RP_DEV Welford chan(Welford a, Welford b) {
+  if (b.n == 0.0) return a;
+  if (a.n == 0.0) return b;
+  const double n = a.n + b.n;
+  const double delta = b.mean - a.mean;
+  Welford r;
+  r.n = n;
+  r.mean = a.mean + delta * (b.n / n);
+  r.m2 = a.m2 + b.m2 + delta * delta * (a.n * b.n / n);
+  return r;
 }
+
+template <int NC, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                 const SParams p) {
+  using L = SLayout<NC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem;
+  uint8_t* sk = smem + L::kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kSmemData);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + L::kStages;
+  uint64_t* q_full = bars + 2 * L::kStages;
+  uint64_t* q_empty = q_full + 1;
+  uint64_t* s_full = q_full + 2;   // [2]
+  uint64_t* s_empty = q_full + 4;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
+  float* knorm_s = reinterpret_cast<float*>(tmem_slot + 4);     // [128]
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(knorm_s + 128);  // [4][128]
+  double* red = reinterpret_cast<double*>(wcnt + 4 * 128);      // [4][3]
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long per = (p.n_items + gridDim.x - 1) / gridDim.x;
+  const long long it0 = static_cast<long long>(blockIdx.x) * per;
+  const long long it1 = min(p.n_items, it0 + per);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      // ------------------------------------------------------ TMA producer
+      const uint64_t pol = policy_evict_normal();
+      uint32_t kv_it = 0, qcnt = 0;
+      int prev_tr = -1;
+      for (long long it = it0; it < it1; ++it) {
+        const ScoreItem item = p.items[it];
+        if (item.tr != prev_tr) {
+          mbar_wait(q_empty, (qcnt & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full, L::kTileBytes);
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            tma_load_3d(sq + c * kChunkBytes, &tq, q_full, (c % p.cph) * 64, c / p.cph,
+                        item.tr * 128, pol);
+          ++qcnt;
+          prev_tr = item.tr;
+        }
+        const uint32_t st = kv_it % L::kStages;
+        mbar_wait(&kv_empty[st], ((kv_it / L::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], L::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          tma_load_3d(sk + st * L::kTileBytes + c * kChunkBytes, &tk, &kv_full[st],
+                      (c % p.cph) * 64, c / p.cph, item.tc * 128, pol);
+        ++kv_it;
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      const uint32_t idesc = idesc_bf16(128, 128, false, false);
+      const uint32_t qa = smem_u32(sq), kb0 = smem_u32(sk);
+      uint32_t kv_it = 0, qcnt = 0, n = 0;
+      int prev_tr = -1;
+      for (long long it = it0; it < it1; ++it, ++n) {
+        const ScoreItem item = p.items[it];
+        if (item.tr != prev_tr) {
+          if (prev_tr >= 0) umma_commit(q_empty);  // old Q' no longer read
+          mbar_wait(q_full, qcnt & 1);
+          ++qcnt;
+          prev_tr = item.tr;
+        }
+        const uint32_t st = kv_it % L::kStages;
+        const uint32_t buf = n & 1;
+        mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
+        mbar_wait(&s_empty[buf], ((n >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kb = kb0 + st * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < NC * 4; ++kk) {
+          const uint32_t off = (kk / 4) * kChunkBytes + (kk % 4) * 32;
+          umma_ss(tmem + buf * 128, smem_desc_sw128(qa + off, 0, 1024),
+                  smem_desc_sw128(kb + off, 0, 1024), idesc, kk > 0);
+        }
+        umma_commit(&kv_empty[st]);
+        umma_commit(&s_full[buf]);
+        ++kv_it;
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue
+    const int r = warp * 32 + lane;  // row within the tile
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    uint32_t n = 0;
+    for (long long it = it0; it < it1; ++it, ++n) {
+      const ScoreItem item = p.items[it];
+      const DJob jb = p.jobs[item.job];
+      const uint32_t buf = n & 1;
+      if (MODE == 1) knorm_s[r] = __ldg(p.knorm + static_cast<long long>(item.tc) * 128 + r);
+      mbar_wait(&s_full[buf], (n >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(trow + buf * 128 + c * 32, sv[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[buf]);
+      // valid columns of this row: contiguous [c_lo, c_hi] (band + frames)
+      const long long gr = static_cast<long long>(item.tr) * 128 + r;
+      const long long qi = static_cast<long long>(jb.i) * p.nt;
+      const long long kj = static_cast<long long>(jb.j) * p.nt;
+      const long long u = gr - qi;
+      int c_lo = 1, c_hi = 0;
+      if (u >= 0 && u < p.nt) {
+        const long long vlo = max(0ll, u - jb.width), vhi = min(static_cast<long long>(p.nt) - 1, u + jb.width);
+        const long long g0 = static_cast<long long>(item.tc) * 128;
+        c_lo = static_cast<int>(max(kj + vlo - g0, 0ll));
+        c_hi = static_cast<int>(min(kj + vhi - g0, 127ll));
+      }
+      if (MODE == 0) {
+        // two-pass (n, mean, M2) over this row's valid scores
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          const float s = __uint_as_float(sv[c / 32][c % 32]) * p.score_scale;
+          if (c >= c_lo && c <= c_hi) sum += s;
+        }
+        const int cnt = c_hi >= c_lo ? c_hi - c_lo + 1 : 0;
+        const float mean = cnt ? sum / static_cast<float>(cnt) : 0.f;
+        float m2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          const float d = __uint_as_float(sv[c / 32][c % 32]) * p.score_scale - mean;
+          if (c >= c_lo && c <= c_hi) m2 = fmaf(d, d, m2);
+        }
+        Welford w{static_cast<double>(cnt), static_cast<double>(mean), static_cast<double>(m2)};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          Welford x{__shfl_xor_sync(0xFFFFFFFFu, w.n, o), __shfl_xor_sync(0xFFFFFFFFu, w.mean, o),
+                    __shfl_xor_sync(0xFFFFFFFFu, w.m2, o)};
+          w = (lane & o) ? chan(x, w) : chan(w, x);  // fixed order -> deterministic
+        }
+        if (lane == 0) {
+          red[warp * 3 + 0] = w.n;
+          red[warp * 3 + 1] = w.mean;
+          red[warp * 3 + 2] = w.m2;
+        }
+        epi_bar();
+        if (r == 0) {
+          Welford a{red[0], red[1], red[2]};
+          for (int x = 1; x < 4; ++x) a = chan(a, Welford{red[3 * x], red[3 * x + 1], red[3 * x + 2]});
+          p.item_stats[3 * it + 0] = a.n;
+          p.item_stats[3 * it + 1] = a.mean;
+          p.item_stats[3 * it + 2] = a.m2;
+        }
+        epi_bar();
+      } else {
+        const double2 st = p.job_stats[item.job];
+        const double invd = 1.0 / (st.y + 1e-8);
+        const float muf = static_cast<float>(st.x);
+        const float inv = static_cast<float>(invd);
+        const float tau = static_cast<float>(jb.param);
+        const float qn = __ldg(p.qnorm + gr) * p.kappa * p.score_scale * inv;
+        epi_bar();  // knorm_s ready
+        uint32_t keep[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          if (c < c_lo || c > c_hi) continue;
+          const float s = __uint_as_float(sv[c / 32][c % 32]) * p.score_scale;
+          const float z = (s - muf) * inv;
+          // error bound in z units: accumulation bound + mu/sigma/rounding floor
+          const float bound = fmaf(qn, knorm_s[c], p.delta_floor * (1.f + fabsf(z)));
+          const float dz = z - tau;
+          if (dz >= bound) {
+            keep[c / 32] |= 1u << (c % 32);
+          } else if (dz > -bound) {
+            const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 + c - kj);
+            const unsigned long long slot = atomicAdd(p.queue_len, 1ull);
+            if (slot < static_cast<unsigned long long>(p.queue_cap)) {
+              p.queue[slot] = make_int4(item.job, static_cast<int>(u), v, 0);
+            } else if (zscore(exact_score(p.feat, gr, kj + v), st) >= jb.param) {
+              keep[c / 32] |= 1u << (c % 32);  // queue full: decide exactly here
+            }
+          }
+        }
+        // per-column counts within each warp (32 rows), then per block row
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const uint32_t b = __ballot_sync(0xFFFFFFFFu, (keep[w4] >> c) & 1u);
+            if (lane == c) wcnt[warp * 128 + w4 * 32 + c] = __popc(b);
+          }
+        }
+        epi_bar();
+        // thread r owns column r: sum the warps of each block row
+        const int bs = p.bs;
+        const int rows_per_blk = bs < 128 ? bs : 128;  // bs in {32, 64, 128}
+        const int wpb = rows_per_blk / 32;             // warps per block row
+        unsigned long long kept_total = 0;
+        const long long gc = static_cast<long long>(item.tc) * 128 + r;
+        for (int br = 0; br < 128 / rows_per_blk; ++br) {
+          uint32_t cnt = 0;
+          for (int x = 0; x < wpb; ++x) cnt += wcnt[(br * wpb + x) * 128 + r];
+          kept_total += cnt;
+          const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
+          const long long Cb = gc / bs;
+          const long long rr = R - jb.r0, cc = Cb - jb.c0;
+          if (rr >= 0 && rr < jb.tr && cc >= 0 && cc < jb.tc && cnt)
+            p.counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs] = cnt;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kept_total += __shfl_xor_sync(0xFFFFFFFFu, kept_total, o);
+        if (lane == 0 && kept_total) atomicAdd(&p.job_kept[item.job], kept_total);
+        epi_bar();  // wcnt / knorm_s reuse
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+// Per-token L2 norm of the concatenated scoring features (H_f heads x d).
+__global__ void norm_kernel(const __nv_bfloat16* __restrict__ x, long long tokens,
+                            long long ts, long long hs, int heads, int d,
+                            float* __restrict__ out) {
+  const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (t >= tokens) return;
+  float acc = 0.f;
+  for (int h = 0; h < heads; ++h)
+    for (int e = lane; e < d; e += 32) {
+      const float v = __bfloat162float(x[t * ts + h * hs + e]);
+      acc = fmaf(v, v, acc);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if (lane == 0) out[t] = sqrtf(acc);
+}
+
+// Deterministic per-frame-pair merge of item statistics (fixed item order).
+__global__ void job_stats_kernel(const double* __restrict__ item_stats,
+                                 const long long* __restrict__ job_item_off, int n_jobs,
+                                 double2* __restrict__ job_stats) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_jobs) return;
+  Welford a{0.0, 0.0, 0.0};
+  for (long long it = job_item_off[j]; it < job_item_off[j + 1]; ++it)
+    a = chan(a, Welford{item_stats[3 * it], item_stats[3 * it + 1], item_stats[3 * it + 2]});
+  const double sd = a.n > 0 ? sqrt(a.m2 / a.n) : 0.0;
+  job_stats[j] = make_double2(a.mean, sd);
+}
+
+// Exact re-score of every queued pair (reference operation order).
+__global__ void recheck_kernel(const DJob* __restrict__ jobs, const int4* __restrict__ queue,
+                               const unsigned long long* __restrict__ queue_len, long long cap,
+                               Feat f, const double2* __restrict__ job_stats, uint32_t* counts,
+                               unsigned long long* job_kept, int nt, int bs) {
+  const long long n = min(static_cast<long long>(*queue_len), cap);
+  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int4 e = queue[x];
+    const DJob& jb = jobs[e.x];
+    const float s = exact_score(f, static_cast<int64_t>(jb.i) * nt + e.y,
+                                static_cast<int64_t>(jb.j) * nt + e.z);
+    if (zscore(s, job_stats[e.x]) >= jb.param) {
+      add_count(jb, counts, nt, bs, e.y, e.z);
+      atomicAdd(&job_kept[e.x], 1ull);
+    }
+  }
+}
+
+// Exact fallback for frame pairs that kept nothing: exact scores of the
+// whole band, then the fallback_k best z (ties to the lowest flat index).
+__global__ void fb_scores_kernel(const DJob* __restrict__ jobs, int job, Feat f, int nt,
+                                 float* __restrict__ scores) {
+  const DJob& jb = jobs[job];
+  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < jb.n;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int64_t u, v;
+    band_uv(x, nt, jb.width, &u, &v);
+    scores[x] = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
+                            static_cast<int64_t>(jb.j) * nt + v);
+  }
+}
+
+__global__ void fb_select_kernel(const DJob* __restrict__ jobs, int job,
+                                 const float* __restrict__ scores,
+                                 const double2* __restrict__ job_stats, uint32_t* counts, int nt,
+                                 int bs, int fallback_k) {
+  const DJob& jb = jobs[job];
+  const int64_t n = jb.n;
+  const double2 st = job_stats[job];
+  __shared__ double bz[32];
+  __shared__ int64_t bi[32];
+  __shared__ int64_t last_pick;
+  __shared__ double last_z;
+  const int k = static_cast<int>(fallback_k < n ? fallback_k : n);
+  if (threadIdx.x == 0) {
+    last_pick = -1;
+    last_z = INFINITY;
+  }
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    double best = -INFINITY;
+    int64_t besti = -1;
+    for (int64_t x = threadIdx.x; x < n; x += blockDim.x) {
+      const double z = zscore(scores[x], st);
+      const bool after = z < last_z || (z == last_z && x > last_pick);
+      if (!after) continue;
+      if (besti < 0 || z > best || (z == best && x < besti)) {
+        best = z;
+        besti = x;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oz = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xFFFFFFFFu, besti, o);
+      if (oi >= 0 && (besti < 0 || oz > best || (oz == best && oi < besti))) {
+        best = oz;
+        besti = oi;
+      }
+    }
+    if (threadIdx.x % 32 == 0) {
+      bz[threadIdx.x / 32] = best;
+      bi[threadIdx.x / 32] = besti;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
+        if (bi[w] >= 0 && (bi[0] < 0 || bz[w] > bz[0] || (bz[w] == bz[0] && bi[w] < bi[0]))) {
+          bz[0] = bz[w];
+          bi[0] = bi[w];
+        }
+      if (bi[0] >= 0) {
+        int64_t u, v;
+        band_uv(bi[0], nt, jb.width, &u, &v);
+        add_count(jb, counts, nt, bs, u, v);
+      }
+      last_pick = bi[0];
+      last_z = bz[0];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ host side ---
+class FastEngine {
+ public:
+  rp_grid g{};
+  int cmin = 0, amin = 0, heads = 0, dim = 0, nc = 0;
+  std::vector<DJob> jobs;        // score jobs only (cnt_off set)
+  std::vector<ScoreItem> items;
+  std::vector<long long> job_item_off;
+  std::vector<Item> tiles;       // block tiles of every score job (apply)
+  int64_t ncounts = 0;
+  DJob* d_jobs = nullptr;
+  ScoreItem* d_items = nullptr;
+  long long* d_job_item_off = nullptr;
+  Item* d_tiles = nullptr;
+  uint32_t* d_counts = nullptr;
+  double* d_item_stats = nullptr;
+  double2* d_job_stats = nullptr;
+  unsigned long long* d_kept = nullptr;  // [jobs + 1]: per job, then queue length
+  int4* d_queue = nullptr;
+  long long queue_cap = 0;
+  float* d_qn = nullptr;
+  float* d_kn = nullptr;
+
+  ~FastEngine() {
+    for (void* p : {static_cast<void*>(d_jobs), static_cast<void*>(d_items),
+                    static_cast<void*>(d_job_item_off), static_cast<void*>(d_tiles),
+                    static_cast<void*>(d_counts), static_cast<void*>(d_item_stats),
+                    static_cast<void*>(d_job_stats), static_cast<void*>(d_kept),
+                    static_cast<void*>(d_queue), static_cast<void*>(d_qn),
+                    static_cast<void*>(d_kn)})
+      if (p) cudaFree(p);
+  }
+};
+
+bool fast_engine_supported(const rp_grid& g, int head_dim, int heads) {
+  const int bs = g.block_size;
+  if (bs != 32 && bs != 64 && bs != 128) return false;
+  if (head_dim % 64 != 0 || heads < 1) return false;
+  const int nc = heads * head_dim / 64;
+  return nc >= 1 && nc <= 4;
+}
+
+template <class T>
+static void dalloc(T** p, size_t n) {
+  RP_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * std::max<size_t>(n, 1)));
+}
+
+FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, int cmin,
+                               int amin, int heads, int head_dim, cudaStream_t s) {
+  (void)s;
+  std::unique_ptr<FastEngine> e(new FastEngine);
+  e->g = g;
+  e->cmin = cmin;
+  e->amin = amin;
+  e->heads = heads;
+  e->dim = head_dim;
+  e->nc = heads * head_dim / 64;
+  const int64_t nt = g.tokens_per_frame;
+  const int bs = g.block_size;
+  int64_t off = 0;
+  for (const DJob& d0 : all) {
+    if (d0.kind != plan::kScore) continue;
+    DJob d = d0;
+    d.cnt_off = off;
+    off += static_cast<int64_t>(d.tr) * d.tc * bs;
+    const int job = static_cast<int>(e->jobs.size());
+    e->jobs.push_back(d);
+    e->job_item_off.push_back(static_cast<long long>(e->items.size()));
+    // 128-token tiles intersecting the band of frames (i, j)
+    const int64_t qi = d.i * nt, kj = d.j * nt;
+    const int64_t tr0 = qi / 128, tr1 = (qi + nt - 1) / 128;
+    const int64_t tc0 = kj / 128, tc1 = (kj + nt - 1) / 128;
+    for (int64_t tr = tr0; tr <= tr1; ++tr) {
+      const int64_t ua = std::max<int64_t>(tr * 128, qi) - qi;
+      const int64_t ub = std::min<int64_t>(tr * 128 + 127, qi + nt - 1) - qi;
+      for (int64_t tc = tc0; tc <= tc1; ++tc) {
+        const int64_t va = std::max<int64_t>(tc * 128, kj) - kj;
+        const int64_t vb = std::min<int64_t>(tc * 128 + 127, kj + nt - 1) - kj;
+        if (va - ub > d.width || ua - vb > d.width) continue;  // no |u - v| <= w
+        e->items.push_back(ScoreItem{job, static_cast<int32_t>(tr), static_cast<int32_t>(tc), 0});
+      }
+    }
+    for (int32_t r = 0; r < d.tr; ++r)
+      for (int32_t c = 0; c < d.tc; ++c) e->tiles.push_back(Item{job, r, c});
+  }
+  e->job_item_off.push_back(static_cast<long long>(e->items.size()));
+  e->ncounts = off;
+  const size_t nj = e->jobs.size();
+  dalloc(&e->d_jobs, nj);
+  dalloc(&e->d_items, e->items.size());
+  dalloc(&e->d_job_item_off, nj + 1);
+  dalloc(&e->d_tiles, e->tiles.size());
+  dalloc(&e->d_counts, static_cast<size_t>(off));
+  dalloc(&e->d_item_stats, 3 * e->items.size());
+  dalloc(&e->d_job_stats, nj);
+  dalloc(&e->d_kept, nj + 1);
+  // recheck queue: 1% of the scored pairs (expected ~0.1%); pairs beyond
+  // the capacity are re-scored in place by the select pass.
+  int64_t pairs = 0;
+  for (const DJob& d : e->jobs) pairs += d.n;
+  e->queue_cap = std::min<int64_t>(std::max<int64_t>(1 << 20, pairs / 100), int64_t{1} << 27);
+  dalloc(&e->d_queue, static_cast<size_t>(e->queue_cap));
+  dalloc(&e->d_qn, static_cast<size_t>(g.padded_tokens));
+  dalloc(&e->d_kn, static_cast<size_t>(g.padded_tokens));
+  RP_CUDA(cudaMemcpy(e->d_jobs, e->jobs.data(), sizeof(DJob) * nj, cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(e->d_items, e->items.data(), sizeof(ScoreItem) * e->items.size(),
+                     cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(e->d_job_item_off, e->job_item_off.data(), sizeof(long long) * (nj + 1),
+                     cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(e->d_tiles, e->tiles.data(), sizeof(Item) * e->tiles.size(),
+                     cudaMemcpyHostToDevice));
+  return e.release();
+}
+
+void fast_engine_destroy(FastEngine* e) { delete e; }
+
+template <int NC>
+static void launch_pass(const CUtensorMap& mq, const CUtensorMap& mk, const SParams& p, int mode,
+                        int grid, cudaStream_t s) {
+  const int smem = SLayout<NC>::kSmemBytes;
+  if (mode == 0) {
+    static bool attr = false;
+    if (!attr) {
+      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 0>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    score_kernel<NC, 0><<<grid, kThreads, smem, s>>>(mq, mk, p);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    score_kernel<NC, 1><<<grid, kThreads, smem, s>>>(mq, mk, p);
+  }
+  RP_LAUNCHED();
+}
+
+void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, const Feat& f,
+                     uint32_t* words, cudaStream_t s, double delta_floor, int fallback_k,
+                     bool want_stats, FastResult* res) {
+  const rp_grid& g = e->g;
+  const int nj = static_cast<int>(e->jobs.size());
+  if (nj == 0 || e->items.empty()) return;
+  // views restricted to the scoring heads
+  rp_tensor qv = *q, kv = *k;
+  qv.heads = e->heads;
+  kv.heads = e->heads;
+  const CUtensorMap mq = make_map_bf16(qv), mk = make_map_bf16(kv);
+  RP_CUDA(cudaMemsetAsync(e->d_counts, 0, sizeof(uint32_t) * std::max<int64_t>(e->ncounts, 1), s));
+  RP_CUDA(cudaMemsetAsync(e->d_kept, 0, sizeof(unsigned long long) * (nj + 1), s));
+  RP_CUDA(cudaMemsetAsync(e->d_qn, 0, sizeof(float) * g.padded_tokens, s));
+  RP_CUDA(cudaMemsetAsync(e->d_kn, 0, sizeof(float) * g.padded_tokens, s));
+  const unsigned ngrid = static_cast<unsigned>((g.total_tokens + 7) / 8);
+  norm_kernel<<<ngrid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(q->data), g.total_tokens,
+                                    q->token_stride, q->head_stride, e->heads, e->dim, e->d_qn);
+  RP_LAUNCHED();
+  norm_kernel<<<ngrid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k->data), g.total_tokens,
+                                    k->token_stride, k->head_stride, e->heads, e->dim, e->d_kn);
+  RP_LAUNCHED();
+
+  SParams p{};
+  p.jobs = e->d_jobs;
+  p.items = e->d_items;
+  p.n_items = static_cast<long long>(e->items.size());
+  p.nt = g.tokens_per_frame;
+  p.bs = g.block_size;
+  p.cph = e->dim / 64;
+  p.score_scale = static_cast<float>((1.0 / std::sqrt(static_cast<double>(e->dim))) / e->heads);
+  p.item_stats = e->d_item_stats;
+  p.job_stats = e->d_job_stats;
+  p.counts = e->d_counts;
+  p.job_kept = e->d_kept;
+  p.queue = e->d_queue;
+  p.queue_len = e->d_kept + nj;
+  p.queue_cap = e->queue_cap;
+  p.qnorm = e->d_qn;
+  p.knorm = e->d_kn;
+  // fp32 accumulation of K = H_f * d exact bf16 products, each rounding
+  // (or truncating) step off by <= 2^-23 relative: |err| <= 2 K 2^-23
+  // sum|q k| <= 2 K 2^-23 |q| |k|.
+  p.kappa = static_cast<float>(2.0 * e->heads * e->dim * std::ldexp(1.0, -23));
+  p.delta_floor = static_cast<float>(delta_floor);
+  p.feat = f;
+  int dev = 0, sms = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = static_cast<int>(std::min<long long>(p.n_items, sms));
+  for (int mode = 0; mode < 2; ++mode) {
+    switch (e->nc) {
+      case 1: launch_pass<1>(mq, mk, p, mode, grid, s); break;
+      case 2: launch_pass<2>(mq, mk, p, mode, grid, s); break;
+      case 3: launch_pass<3>(mq, mk, p, mode, grid, s); break;
+      default: launch_pass<4>(mq, mk, p, mode, grid, s); break;
+    }
+    if (mode == 0) {
+      job_stats_kernel<<<(nj + 127) / 128, 128, 0, s>>>(e->d_item_stats, e->d_job_item_off, nj,
+                                                       e->d_job_stats);
+      RP_LAUNCHED();
+    }
+  }
+  // exact re-score of the pairs within their error bound of tau; the
+  // queue length is read on the device (no host sync)
+  {
+    recheck_kernel<<<sms * 8, 256, 0, s>>>(e->d_jobs, e->d_queue, e->d_kept + nj, e->queue_cap,
+                                         f, e->d_job_stats, e->d_counts, e->d_kept,
+                                         g.tokens_per_frame, g.block_size);
+    RP_LAUNCHED();
+  }
+  // fallback_k: only when it can activate a column (fallback_k >= cmin)
+  const bool fb_matters = fallback_k >= e->cmin;
+  std::vector<unsigned long long> kept;
+  if (fb_matters || want_stats) {
+    kept.resize(nj + 1);
+    RP_CUDA(cudaMemcpyAsync(kept.data(), e->d_kept, sizeof(unsigned long long) * (nj + 1),
+                            cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    if (res) res->rechecked = static_cast<int64_t>(kept[nj]);
+    for (int j = 0; j < nj; ++j) {
+      if (kept[j] != 0) continue;
+      if (res) ++res->fallbacks;
+      if (!fb_matters) continue;
+      float* sc = nullptr;
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), sizeof(float) * e->jobs[j].n, s));
+      fb_scores_kernel<<<std::min<int64_t>((e->jobs[j].n + 255) / 256, 4096), 256, 0, s>>>(
+          e->d_jobs, j, f, g.tokens_per_frame, sc);
+      RP_LAUNCHED();
+      fb_select_kernel<<<1, 256, 0, s>>>(e->d_jobs, j, sc, e->d_job_stats, e->d_counts,
+                                         g.tokens_per_frame, g.block_size, fallback_k);
+      RP_LAUNCHED();
+      RP_CUDA(cudaFreeAsync(sc, s));
+    }
+  }
+  // theta_c / theta_m per block tile of every scored frame pair
+  const int64_t chunk = int64_t{1} << 30;
+  for (int64_t b = 0; b < static_cast<int64_t>(e->tiles.size()); b += chunk) {
+    const int64_t n = std::min<int64_t>(chunk, e->tiles.size() - b);
+    const int th = g.block_size >= 1024 ? 1024 : (g.block_size < 32 ? 32 : g.block_size);
+    apply_kernel<<<static_cast<unsigned>(n), th, 0, s>>>(e->d_jobs, e->d_tiles + b, e->d_counts,
+                                                         words, g.tokens_per_frame,
+                                                         g.block_size, g.row_bytes, e->cmin,
+                                                         e->amin, 1);
+    RP_LAUNCHED();
+  }
+}
+
 }  // namespace mask
 }  // namespace rp
