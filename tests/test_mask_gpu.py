@@ -98,3 +98,35 @@ def test_dynamic_needs_features(cuda):
     g = rp.make_grid(4, 16, 4)
     with pytest.raises(rp.InvalidArgument, match="dynamic mode needs features"):
         rp.build_mask(g, rp.SparsityConfig(rp.Mode.DynamicThreshold), 1)
+
+
+# ------------------------------------------------ tensor-core dynamic engine
+FAST_CASES = [
+    # nf, nt, bs, hf, d, cfg
+    (8, 256, 128, 2, 64, Cfg(1, 1.4, 0.7, 1e-6, 0.7, 0.45, 0.0, 0.0)),
+    (8, 256, 32, 2, 64, Cfg(1, 1.4, 0.7, 1e-6, 0.7, 0.45, -1.5, 2.0)),
+    (8, 256, 64, 2, 64, Cfg(1, 1.4, 0.7, 1e-6, 0.7, 0.45, 0.05, 0.05)),
+    (6, 500, 128, 2, 128, Cfg(1, 2.0, 0.5, 1e-6, 0.5, 0.3, 0.5, 1.0)),
+    (6, 500, 64, 1, 128, Cfg(1, 1.0, 1.0, 1e-6, 0.3, 0.2, -0.5, 0.8)),
+    (8, 512, 128, 2, 128, Cfg(1, 1.4, 0.7, 1e-6, 0.7, 0.45, -1.5, 2.0)),
+]
+
+
+@pytest.mark.parametrize("case", FAST_CASES, ids=lambda c: f"{c[0]}x{c[1]}-B{c[2]}-hf{c[3]}-d{c[4]}")
+def test_fast_engine_matches_reference(cuda, port, case):
+    """bf16 features: tensor-core scores + exact fp64 recheck near tau vs the
+    reference algorithm on the same (bf16-valued) features."""
+    nf, nt, bs, hf, d, c = case
+    q, k, _ = port.random_batch(nf * nt, hf, d, 42, with_values=False, threads=8)
+    qb = torch.from_numpy(q).to(torch.bfloat16)
+    kb = torch.from_numpy(k).to(torch.bfloat16)
+    want = port.build_mask(nf, nt, bs, c, 7, False, qb.float().numpy(), kb.float().numpy(),
+                           threads=8)
+    st = {}
+    got = gpu_mask(nf, nt, bs, c, 7, False, qb.float().numpy(), kb.float().numpy(),
+                   dtype=torch.bfloat16, engine=1, stats=st)
+    exact = gpu_mask(nf, nt, bs, c, 7, False, qb.float().numpy(), kb.float().numpy(),
+                     dtype=torch.bfloat16, engine=2)
+    assert np.array_equal(exact, want)
+    assert np.array_equal(got, want), int((got != want).sum())
+    assert st["rechecked_pairs"] < 0.05 * max(st["scored_pairs"], 1)
