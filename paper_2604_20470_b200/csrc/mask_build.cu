@@ -643,6 +643,7 @@ rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
       }
       RP_CUDA(cudaMemcpyAsync(mask_bits_dev, P->cached.p, bytes, cudaMemcpyDeviceToDevice, s));
     } else {
+      P->scored = 0;  // BuildTimings::scored_pairs of this build
       DevBuf<uint32_t> work(P->words, s);
       RP_CUDA(cudaMemcpyAsync(work.p, P->base.p, P->words * 4, cudaMemcpyDeviceToDevice, s));
       const Feat f = make_feat(q, k, n_score_heads);
@@ -663,6 +664,8 @@ rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
           P->fast_heads = n_score_heads;
           P->fast_dim = q->head_dim;
         }
+        for (const DJob& d : P->djobs)
+          if (d.kind == plan::kScore) P->scored += d.n;
         FastResult fr;
         fast_engine_run(P->fast, q, k, f, work.p, s,
                         P->o.recheck_delta > 0 ? P->o.recheck_delta : 1e-5, P->c.fallback_k,
