@@ -1,0 +1,221 @@
+// TEST INFRASTRUCTURE — GPU parity of the C++ facade against the reference's
+// own brute-force oracle (proj/tests/oracle.cpp, compiled unmodified against
+// the facade headers by oracle/Makefile target `facade`).
+//
+//   * build_mask vs oracle::build on the SPEC acceptance-criterion-1 sweep
+//     (N_f in {2..6}, N_t in {4,8,12}, B = 4, random Table-5
+//     configs per mode, random seeds, fallback_k in {1,2,3}) plus tiny
+//     golden-shape configs at B in {16, 32, 64, 128}: bit-identical masks
+//     (oracle::same_mask).
+//   * static_select / proxy_scores / normalize_scores / dynamic_select vs
+//     oracle::pick_static / score_pairs / standardize / pick_dynamic:
+//     identical pair lists, bit-identical scores and z values.
+//   * masked_attention_exact (fp32) vs a brute-force double evaluation of
+//     attention.cpp:50-106 over the expanded mask, within 1e-5.
+// Exit code 0 iff everything matches; prints one summary line.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "oracle.hpp"
+#include "radialplan/mask.hpp"
+
+using namespace radialplan;
+
+namespace {
+
+int g_fail = 0;
+#define EXPECT(cond, ...)                                                      \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      ++g_fail;                                                                \
+      std::fprintf(stderr, "FAIL %s:%d: ", __FILE__, __LINE__);                \
+      std::fprintf(stderr, __VA_ARGS__);                                       \
+      std::fprintf(stderr, "\n");                                              \
+    }                                                                          \
+  } while (0)
+
+SparsityConfig random_config(std::mt19937_64& r, Mode mode) {
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  SparsityConfig c;
+  c.mode = mode;
+  c.radial.decay_factor = 0.5 + 1.5 * u01(r);        // Table 5: gamma in [0.5, 2]
+  c.radial.long_range_factor = 0.05 + 0.95 * u01(r);  // lambda in (0, 1]
+  c.mask_threshold = 0.1 + 0.9 * u01(r);
+  c.col_threshold = 0.1 + 0.9 * u01(r);
+  if (mode == Mode::StaticRatio) {
+    c.near_param = 0.05 + 0.95 * u01(r);
+    c.far_param = 0.05 + 0.95 * u01(r);
+  } else {
+    c.near_param = -10.0 + 15.0 * u01(r);  // PAPER.md:603-604 BO ranges
+    c.far_param = -5.0 + 13.0 * u01(r);
+  }
+  c.fallback_k = 1 + static_cast<int>(r() % 3);
+  return c;
+}
+
+int check_mask(const GridSpec& g, const SparsityConfig& c, std::uint64_t seed,
+               const FeatureBatch* f, bool no_split) {
+  BuildOptions o;
+  o.features = f;
+  o.disable_split = no_split;
+  const BlockMask ours = build_mask(g, c, seed, o);
+  const oracle::Grid og = oracle::grid(g.n_frames, g.tokens_per_frame, g.block_size);
+  const oracle::DenseMask want = oracle::build(og, c, f, seed, no_split);
+  const bool same = oracle::same_mask(want, ours);
+  EXPECT(same, "mask mismatch nf=%d nt=%d B=%d mode=%d seed=%llu", g.n_frames,
+         g.tokens_per_frame, g.block_size, static_cast<int>(c.mode),
+         static_cast<unsigned long long>(seed));
+  return same ? 1 : 0;
+}
+
+void selection_ops(std::mt19937_64& r, int& cases) {
+  for (int rep = 0; rep < 40; ++rep) {
+    const int nf = 2 + static_cast<int>(r() % 4), nt = 4 + 4 * static_cast<int>(r() % 6);
+    const GridSpec g = make_grid(nf, nt, 4);
+    const FeatureBatch f = random_batch(g.total_tokens, 1 + static_cast<int>(r() % 2),
+                                        4 + 4 * static_cast<int>(r() % 4), r(), false);
+    RadialParams p;
+    p.decay_factor = 0.3 + r() % 100 / 60.0;
+    p.long_range_factor = 1.0;
+    const int i = static_cast<int>(r() % nf), j = static_cast<int>(r() % nf);
+    const CandidateSet cs = candidate_set(i, j, p, g);
+    if (cs.pair_count() == 0) continue;
+    const oracle::Grid og = oracle::grid(nf, nt, 4);
+    const auto pairs = oracle::band_pairs(og, cs.width);
+    // static_select vs pick_static
+    const double ratio = 0.05 + (r() % 90) / 100.0;
+    const std::uint64_t seed = r();
+    const auto got = static_select(cs, ratio, seed);
+    const auto want = oracle::pick_static(pairs, ratio, pair_seed(seed, i, j));
+    bool same = got.size() == want.size();
+    for (std::size_t x = 0; same && x < got.size(); ++x)
+      same = got[x].first == want[x].first && got[x].second == want[x].second;
+    EXPECT(same, "static_select mismatch rep=%d", rep);
+    // proxy_scores vs score_pairs (bit-identical floats)
+    const auto s = proxy_scores(f, i, j, cs, nt);
+    const auto so = oracle::score_pairs(f, i, j, nt, pairs);
+    EXPECT(s.size() == so.size() && std::memcmp(s.data(), so.data(), s.size() * 4) == 0,
+           "proxy_scores mismatch rep=%d", rep);
+    // normalize_scores vs standardize (bit-identical doubles)
+    ScoreStats st;
+    const auto z = normalize_scores(s, &st);
+    const auto zo = oracle::standardize(so);
+    EXPECT(z.size() == zo.size() && std::memcmp(z.data(), zo.data(), z.size() * 8) == 0,
+           "normalize_scores mismatch rep=%d", rep);
+    // dynamic_select vs pick_dynamic, including the fallback branch
+    for (double tau : {-0.5, 0.7, 50.0}) {
+      const int fk = 1 + static_cast<int>(r() % 3);
+      const auto d = dynamic_select(cs, z, tau, fk);
+      const auto dw = oracle::pick_dynamic(pairs, zo, tau, fk);
+      bool eq = d.size() == dw.size();
+      for (std::size_t x = 0; eq && x < d.size(); ++x)
+        eq = d[x].first == dw[x].first && d[x].second == dw[x].second;
+      EXPECT(eq, "dynamic_select mismatch rep=%d tau=%g", rep, tau);
+    }
+    ++cases;
+  }
+}
+
+// attention.cpp:50-106 (exact variant) by brute force in double.
+double attention_check(const FeatureBatch& b, const TokenMask& m) {
+  const auto out = masked_attention_exact(b, m);
+  const std::int64_t n = m.dim;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(b.head_dim));
+  double worst = 0.0;
+  std::vector<double> p(static_cast<std::size_t>(n));
+  for (int h = 0; h < b.heads; ++h) {
+    const auto at = [&](const Eigen::MatrixXf& x, std::int64_t t, int e) {
+      return t < b.tokens ? static_cast<double>(x(t, e)) : 0.0;
+    };
+    for (std::int64_t r = 0; r < n; ++r) {
+      double mx = -INFINITY;
+      for (std::int64_t c = 0; c < n; ++c) {
+        if (!m.get(r, c)) {
+          p[static_cast<std::size_t>(c)] = -INFINITY;
+          continue;
+        }
+        float dot = 0.0f;  // logits: float GEMM in the reference
+        for (int e = 0; e < b.head_dim; ++e)
+          dot += static_cast<float>(at(b.queries[h], r, e) * at(b.keys[h], c, e));
+        p[static_cast<std::size_t>(c)] = dot * scale;
+        mx = std::max(mx, p[static_cast<std::size_t>(c)]);
+      }
+      double sum = 0.0;
+      for (auto& x : p) {
+        x = std::isinf(x) ? 0.0 : std::exp(x - mx);
+        sum += x;
+      }
+      for (int e = 0; e < b.head_dim; ++e) {
+        double acc = 0.0;
+        for (std::int64_t c = 0; c < n; ++c) acc += p[static_cast<std::size_t>(c)] * at(b.values[h], c, e);
+        const double want = acc / sum;
+        worst = std::max(worst, std::fabs(want - out[static_cast<std::size_t>(h)](r, e)));
+      }
+    }
+  }
+  return worst;
+}
+
+}  // namespace
+
+int main() {
+  std::mt19937_64 r(20260417);
+  int masks = 0, ops = 0;
+  // SPEC criterion 1, both modes.
+  for (Mode mode : {Mode::StaticRatio, Mode::DynamicThreshold})
+    for (int nf = 2; nf <= 6; ++nf)
+      for (int nt : {4, 8, 12})
+        for (int rep = 0; rep < 10; ++rep) {
+          const GridSpec g = make_grid(nf, nt, 4);
+          const SparsityConfig c = random_config(r, mode);
+          const FeatureBatch f = random_batch(g.total_tokens, 2, 8, r(), false);
+          masks += check_mask(g, c, r(), mode == Mode::DynamicThreshold ? &f : nullptr,
+                              rep % 5 == 4 && mode == Mode::DynamicThreshold);
+        }
+  // Tiny golden shape (8 x 16 x 16 = 2048 tokens), B in {16, 32, 64, 128}.
+  const FeatureBatch tiny = random_batch(2048, 2, 64, 42, false);
+  for (int bs : {16, 32, 64, 128}) {
+    const GridSpec g = make_grid(8, 256, bs);
+    SparsityConfig st;
+    st.radial.decay_factor = 2.0;
+    st.radial.long_range_factor = bs == 32 ? 0.3 : 1.0;
+    st.near_param = st.far_param = 0.22;
+    masks += check_mask(g, st, 7, nullptr, false);
+    SparsityConfig dy;
+    dy.mode = Mode::DynamicThreshold;
+    dy.radial.decay_factor = 1.4;
+    dy.radial.long_range_factor = 0.7;
+    dy.mask_threshold = 0.7;
+    dy.col_threshold = 0.45;
+    for (double tau : {0.0, 0.05, 0.08}) {
+      dy.near_param = dy.far_param = tau;
+      masks += check_mask(g, dy, 7, &tiny, false);
+    }
+  }
+  selection_ops(r, ops);
+  // Stage (d): expanded block masks, padded grid (8 x 250, B = 32: 16 pad
+  // tokens attended as zero keys), all-ones and single-block rows.
+  double worst = 0.0;
+  {
+    const GridSpec g = make_grid(2, 100, 32);
+    const FeatureBatch b = random_batch(g.total_tokens, 2, 16, 11, true);
+    SparsityConfig c;
+    c.near_param = c.far_param = 0.3;
+    const BlockMask bm = build_mask(g, c, 3, {});
+    worst = std::max(worst, attention_check(b, expand_mask(bm, g)));
+    BlockMask ones(g.blocks_per_dim);
+    for (std::int64_t x = 0; x < g.blocks_per_dim; ++x)
+      for (std::int64_t y = 0; y < g.blocks_per_dim; ++y) ones.set(x, y);
+    worst = std::max(worst, attention_check(b, expand_mask(ones, g)));
+    BlockMask diag(g.blocks_per_dim);
+    for (std::int64_t x = 0; x < g.blocks_per_dim; ++x) diag.set(x, x);
+    worst = std::max(worst, attention_check(b, expand_mask(diag, g)));
+  }
+  EXPECT(worst < 1e-5, "masked_attention_exact max abs error %.3g", worst);
+  std::printf("[parity_oracle] masks bit-identical %d, selection-op cases %d, attention max abs "
+              "err %.3g, failures %d\n",
+              masks, ops, worst, g_fail);
+  return g_fail ? 1 : 0;
+}

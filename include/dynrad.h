@@ -2,9 +2,9 @@
  *
  * This is the drop-in boundary.  The reference (arxiv/paper_2604_20470,
  * `radialplan`) exposes the path as a C++ library API in namespace
- * radialplan (proj/include/radialplan/*.hpp); it has no extern "C" layer.
+ * radialplan (proj/include/radialplan/ headers); it has no extern "C" layer.
  * Each entry point below names the reference interface it replaces.  The C++
- * facade in include/radialplan_b200/radialplan.hpp re-exposes the reference
+ * facade in include/radialplan_b200/radialplan_b200.hpp re-exposes the reference
  * signatures on top of these calls, and INTEGRATION.md shows the bindings.
  *
  * Conventions
@@ -159,6 +159,56 @@ rp_status rp_build_mask(const rp_grid* g, const rp_config* c, uint64_t seed,
                         const rp_tensor* k, int n_score_heads,
                         uint8_t* mask_bits_dev, rp_build_stats* stats,
                         rp_stream stream);
+
+/* ------------------------------------- per-frame-pair selection operators --
+ * The building blocks build_mask runs fused, exposed one by one with the
+ * reference's semantics (selection.hpp:60-82) for callers that drive the
+ * selection themselves.  A band is one ordered frame pair's candidate set
+ * (radial.hpp:50-73: |u - v| <= width over local in-frame indices, empty
+ * when not retained).  Pair lists are int64 (u, v) pairs in the reference's
+ * output order.  These are synchronous (they return counts to the host). */
+typedef struct {
+  int frame_i;
+  int frame_j;
+  int64_t tokens_per_frame;
+  int64_t width;
+  int retained;
+} rp_band;
+
+/* static_select (selection.cpp:61-91): partial Fisher-Yates of
+ * k = max(1, floor(n * ratio)) flat indices with SplitMix64(pair_seed(seed,
+ * i, j)), in slot order.  uv_dev holds cap pairs; *count = k (0 if the band
+ * is empty).  RP_INVALID_ARGUMENT for ratio outside (0, 1]. */
+rp_status rp_static_select(const rp_band* band, double ratio, uint64_t seed, int64_t* uv_dev,
+                           int64_t cap, int64_t* count, rp_stream stream);
+
+/* proxy_scores (selection.cpp:93-123): s(u,v) = float(sum_h dot_h(q_u, k_v)
+ * / sqrt(d) / H) over the first n_heads heads, fp64 accumulation in the
+ * reference's order (bit-identical); scores_dev holds pair_count floats in
+ * canonical row-major band order. */
+rp_status rp_proxy_scores(const rp_tensor* q, const rp_tensor* k, int n_heads,
+                          const rp_band* band, float* scores_dev, rp_stream stream);
+
+/* normalize_scores (selection.cpp:125-148): sequential population mean /
+ * stddev in fp64 (bit-identical) and z = (s - mean) / (stddev + 1e-8).
+ * n = 0 gives mean = stddev = 0.  mean/stddev are host outputs (may be
+ * NULL). */
+rp_status rp_normalize_scores(const float* scores_dev, int64_t n, double* z_dev, double* mean,
+                              double* stddev, rp_stream stream);
+
+/* dynamic_select (selection.cpp:150-185): pairs with z >= threshold in flat
+ * order; if none, the fallback_k best z (ties to the lower flat index) in
+ * ascending flat order.  n must equal the band's pair count. */
+rp_status rp_dynamic_select(const rp_band* band, const double* z_dev, int64_t n,
+                            double threshold, int fallback_k, int64_t* uv_dev, int64_t cap,
+                            int64_t* count, rp_stream stream);
+
+/* Token-level mask (dim x ceil(dim/8) bytes, the reference's TokenMask
+ * layout) -> block mask at block_size B (dim % B == 0): the block bit of
+ * every B x B block; *uniform = 1 iff every block is constant (the token
+ * mask is an expand_mask of the result).  Synchronous. */
+rp_status rp_token_mask_to_blocks(const uint8_t* token_bits_dev, int64_t dim, int block_size,
+                                  uint8_t* block_bits_dev, int* uniform, rp_stream stream);
 
 /* -------------------------------------------------------- mask utilities --
  * Block-sparse row lists (new; the reference stops at the bitmask):

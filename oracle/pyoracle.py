@@ -234,6 +234,19 @@ class _RefLib(_Lib):
                                             st))
         return s[:n], z[:n], (st[0], st[1])
 
+    def dynamic_select(self, nf, nt, bs, cfg: Cfg, i, j, z, tau, fallback_k):
+        z = np.ascontiguousarray(z, np.float64)
+        n = z.size
+        cap = max(1, n)
+        out = np.zeros((cap, 2), np.int64)
+        kk = C.c_int64()
+        c = cfg.c()
+        self._chk(self.lib.ref_dynamic_select(nf, nt, bs, C.byref(c), i, j,
+                                              z.ctypes.data_as(_P(C.c_double)), n, tau,
+                                              fallback_k, out.ctypes.data_as(_P(C.c_int64)),
+                                              cap, C.byref(kk)))
+        return out[: kk.value]
+
 
 class _PortLib(_Lib):
     def __init__(self, path, kind):

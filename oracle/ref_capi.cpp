@@ -269,4 +269,24 @@ int ref_proxy_scores(int nf, int nt, int bs, const ref_cfg* cfg, int i, int j,
   });
 }
 
+// dynamic_select (selection.cpp:150-185) on given z values.
+int ref_dynamic_select(int nf, int nt, int bs, const ref_cfg* cfg, int i, int j,
+                       const double* z, std::int64_t n, double tau, int fallback_k,
+                       std::int64_t* out_uv, std::int64_t cap, std::int64_t* k_out) {
+  return guarded([&] {
+    GridSpec g = make_grid(nf, nt, bs);
+    SparsityConfig c = to_cfg(cfg);
+    CandidateSet cs = candidate_set(i, j, c.radial, g);
+    std::vector<double> zz(z, z + n);
+    auto sel = dynamic_select(cs, zz, tau, fallback_k);
+    *k_out = static_cast<std::int64_t>(sel.size());
+    if (static_cast<std::int64_t>(sel.size()) > cap)
+      throw std::out_of_range("ref_dynamic_select: capacity");
+    for (std::size_t x = 0; x < sel.size(); ++x) {
+      out_uv[2 * x] = sel[x].first;
+      out_uv[2 * x + 1] = sel[x].second;
+    }
+  });
+}
+
 }  // extern "C"

@@ -111,6 +111,16 @@ class BuildStats(C.Structure):
     ]
 
 
+class Band(C.Structure):
+    _fields_ = [
+        ("frame_i", C.c_int),
+        ("frame_j", C.c_int),
+        ("tokens_per_frame", C.c_int64),
+        ("width", C.c_int64),
+        ("retained", C.c_int),
+    ]
+
+
 RP_F32, RP_BF16 = 0, 1
 
 _lib = None
@@ -139,6 +149,13 @@ _SIGS = {
                                  _v, _v, C.c_float, _v], C.c_int),
     "rp_masked_attention_exact_host": ([_P(Grid), _v, _v, _v, _v, C.c_int, C.c_int64, C.c_int,
                                         C.c_int, _v, _v], C.c_int),
+    "rp_static_select": ([_P(Band), C.c_double, C.c_uint64, _v, C.c_int64, _P(C.c_int64), _v],
+                         C.c_int),
+    "rp_proxy_scores": ([_P(Tensor), _P(Tensor), C.c_int, _P(Band), _v, _v], C.c_int),
+    "rp_normalize_scores": ([_v, C.c_int64, _v, _P(C.c_double), _P(C.c_double), _v], C.c_int),
+    "rp_dynamic_select": ([_P(Band), _v, C.c_int64, C.c_double, C.c_int, _v, C.c_int64,
+                           _P(C.c_int64), _v], C.c_int),
+    "rp_token_mask_to_blocks": ([_v, C.c_int64, C.c_int, _v, _P(C.c_int), _v], C.c_int),
     "rp_debug_umma_probe": ([_v, _v, _v, _v, _v, _v, _v], C.c_int),
 }
 

@@ -43,6 +43,12 @@ constexpr int kBN = 128;  // keys per KV tile (= block size B)
 #define RP_POLY_MASK 0x00u
 #endif
 constexpr uint32_t kPolyMask = RP_POLY_MASK;
+// Keys of P after which the softmax signals the MMA warp (p_split) so that
+// P.V on them overlaps the last chunk's exponentials (multiple of 32, < 128).
+#ifndef RP_SPLIT_KEYS
+#define RP_SPLIT_KEYS 128
+#endif
+constexpr int kSplitKeys = RP_SPLIT_KEYS;
 
 template <int D>
 struct Layout {
@@ -51,11 +57,27 @@ struct Layout {
   static constexpr int kChunkBytes = 128 * 128;    // 128 rows x 128 B
   static constexpr int kStages = D == 128 ? 5 : 10;
   static constexpr int kSmemData = 2 * kTileBytes + kStages * kTileBytes;
-  static constexpr int kNumBars = 2 * kStages + 12;
+  static constexpr int kNumBars = 2 * kStages + 14;
   static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + 1024;
   RP_HD static uint32_t s_col(int x) { return x ? 128u : 0u; }
   RP_HD static uint32_t o_col(int x) { return x ? 384u : 256u; }
 };
+
+#ifdef RP_TRACE
+// Debug-only event trace (tools/trace_k6.py): clock64 stamps of the softmax
+// and MMA roles of the first kTraceCtas CTAs.
+constexpr int kTraceCtas = 4, kTraceEv = 12, kTraceSteps = 512;
+__device__ unsigned long long g_trace[kTraceCtas][kTraceEv][kTraceSteps];
+#define RP_TR(ev, idx)                                                        \
+  do {                                                                        \
+    if (blockIdx.x < kTraceCtas && (idx) < kTraceSteps)                       \
+      g_trace[blockIdx.x][ev][idx] = clock64();                               \
+  } while (0)
+#else
+#define RP_TR(ev, idx) \
+  do {                 \
+  } while (0)
+#endif
 
 struct Params {
   const int32_t* row_ptr;
@@ -89,6 +111,16 @@ RP_DEV Unit decode(const Params& p, long long u) {
   return w;
 }
 
+// decode() for a whole role warp: the row-list lookups are broadcast from
+// lane 0 so every derived value is provably warp-uniform.
+RP_DEV Unit decode_warp(const Params& p, long long u) {
+  Unit w = decode(p, u);
+  w.row = shfl0(w.row);
+  w.beg = shfl0(w.beg);
+  w.n = shfl0(w.n);
+  return w;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     bsfa_fwd_kernel(const __grid_constant__ CUtensorMap tq,
@@ -109,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = q_full + 6;    // softmax -> MMA: P_x written to TMEM
   uint64_t* o_done = q_full + 8;    // MMA -> softmax: unit's last P.V done
   uint64_t* o_free = q_full + 10;   // softmax -> MMA: epilogue read O_x
+  uint64_t* p_split = q_full + 12;  // softmax -> MMA: P_x keys [0, kSplitKeys) written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
 
   const int warp = threadIdx.x / 32;
@@ -126,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&p_full[x], 4);
       mbar_init(&o_done[x], 1);
       mbar_init(&o_free[x], 4);
+      mbar_init(&p_split[x], 4);
     }
     fence_barrier_init();
   }
@@ -146,8 +180,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 2 * 128 * 208 + 128 * 88 == 384 * 168 (an over-ask would block forever).
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
-    if (warp == 8 && lane == 0) {
+    if (warp == 8) {
       // ---------------------------------------------------- TMA producer --
+      // (whole warp, uniform control flow; one elected lane issues)
       const uint64_t pol_q = policy_evict_first();
 #ifdef RP_KV_EVICT_NORMAL
       const uint64_t pol_kv = policy_evict_normal();
@@ -160,32 +195,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t st = kv_it % L::kStages;
         const uint32_t ph = (kv_it / L::kStages) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], L::kTileBytes);
+#ifdef RP_ABL_NOLOAD
+        // ablation: after the ring's first fill, reuse stale tiles (timing only)
+        if (kv_it >= L::kStages) {
+          if (lane == 0) mbar_arrive(&kv_full[st]);
+          ++kv_it;
+          return;
+        }
+#endif
+        mbar_arrive_expect_tx_w(&kv_full[st], L::kTileBytes);
         uint8_t* dst = skv + st * L::kTileBytes;
 #pragma unroll
         for (int c = 0; c < L::kChunks; ++c)
-          tma_load_3d(dst + c * L::kChunkBytes, m, &kv_full[st], c * 64, h, blk * kBN, pol_kv);
+          tma_load_3d_w(dst + c * L::kChunkBytes, m, &kv_full[st], c * 64, h, blk * kBN, pol_kv);
         ++kv_it;
       };
       for (long long u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Unit w = decode(p, u);
+        const Unit w = decode_warp(p, u);
         for (int x = 0; x < 2; ++x) {
           if (x == 1 && !w.has_b) continue;
           mbar_wait(&q_empty[x], (ucnt[x] & 1) ^ 1);
-          mbar_arrive_expect_tx(&q_full[x], L::kTileBytes);
+          mbar_arrive_expect_tx_w(&q_full[x], L::kTileBytes);
 #pragma unroll
           for (int c = 0; c < L::kChunks; ++c)
-            tma_load_3d(sq + x * L::kTileBytes + c * L::kChunkBytes, &tq, &q_full[x], c * 64,
+            tma_load_3d_w(sq + x * L::kTileBytes + c * L::kChunkBytes, &tq, &q_full[x], c * 64,
                         x ? w.h1 : w.h0, w.row * kBM, pol_q);
           ++ucnt[x];
         }
         // order must match the MMA issue order below
         const int32_t* cols = p.col_idx + w.beg;
-        int cj = __ldg(cols);
+        int cj = shfl0(__ldg(cols));
         load_kv(&tk, w.h0, cj);
         if (w.has_b) load_kv(&tk, w.h1, cj);
         for (int j = 0; j < w.n; ++j) {
-          const int cn = j + 1 < w.n ? __ldg(cols + j + 1) : 0;
+          const int cn = j + 1 < w.n ? shfl0(__ldg(cols + j + 1)) : 0;
           load_kv(&tv, w.h0, cj);
           if (j + 1 < w.n) load_kv(&tk, w.h0, cn);
           if (w.has_b) {
@@ -195,8 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           cj = cn;
         }
       }
-    } else if (warp == 9 && lane == 0) {
+    } else if (warp == 9) {
       // ----------------------------------------------------- MMA issuer ---
+      // (whole warp, uniform control flow; one elected lane issues)
       const uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
       const uint32_t idesc_pv = idesc_bf16(128, D, false, true);
       const uint32_t sq_addr = smem_u32(sq);
@@ -214,32 +258,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk / 4) * L::kChunkBytes + (kk % 4) * 32;
-          umma_ss(tmem + L::s_col(x), smem_desc_sw128(qa + off, 0, 1024),
+          umma_ss_w(tmem + L::s_col(x), smem_desc_sw128(qa + off, 0, 1024),
                   smem_desc_sw128(kb + off, 0, 1024), idesc_qk, kk > 0);
         }
-        umma_commit(&kv_empty[st]);
-        umma_commit(&s_full[x]);
-        if (last_s) umma_commit(&q_empty[x]);
+        umma_commit_w(&kv_empty[st]);
+        umma_commit_w(&s_full[x]);
+        if (last_s) umma_commit_w(&q_empty[x]);
         ++kv_it;
       };
       // O_x (+)= P_x . V : 128 x D, K = 128 keys in steps of 16; P in TMEM
       // (bf16 pairs packed in the S_x columns 0..63).
-      auto issue_pv = [&](int x, bool first, bool last) {
+      auto issue_pv = [&](int x, bool first, bool last, uint32_t ph) {
         const uint32_t st = kv_it % L::kStages;
         mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
         tc_fence_after();
         const uint32_t vb = skv_addr + st * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
-          umma_ts(tmem + L::o_col(x), tmem + L::s_col(x) + kk * 8,
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          if (kk == kSplitKeys / 16) {
+            // the tail of P_x: written after the split arrive
+            mbar_wait(&p_full[x], ph);
+            tc_fence_after();
+          }
+          umma_ts_w(tmem + L::o_col(x), tmem + L::s_col(x) + kk * 8,
                   smem_desc_sw128(vb + kk * 16 * 128, L::kChunkBytes, 1024), idesc_pv,
                   (!first) || kk > 0);
-        umma_commit(&kv_empty[st]);
-        if (last) umma_commit(&o_done[x]);
+        }
+        umma_commit_w(&kv_empty[st]);
+        if (last) umma_commit_w(&o_done[x]);
         ++kv_it;
       };
       for (long long u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Unit w = decode(p, u);
+        const Unit w = decode_warp(p, u);
         const int nx = w.has_b ? 2 : 1;
         for (int x = 0; x < nx; ++x) {
           mbar_wait(&q_full[x], ucnt[x] & 1);
@@ -247,11 +297,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int j = 0; j < w.n; ++j) {
           for (int x = 0; x < nx; ++x) {
-            mbar_wait(&p_full[x], pcnt[x] & 1);
+            RP_TR(6 + 2 * x, pcnt[x]);
+            const uint32_t ph = pcnt[x] & 1;
+            mbar_wait(&p_split[x], ph);
+            RP_TR(7 + 2 * x, pcnt[x]);
             ++pcnt[x];
             if (j == 0) mbar_wait(&o_free[x], (ucnt[x] & 1) ^ 1);
             tc_fence_after();
-            issue_pv(x, j == 0, j == w.n - 1);
+            issue_pv(x, j == 0, j == w.n - 1, ph);
             if (j + 1 < w.n) issue_s(x, j + 1 == w.n - 1);
           }
         }
@@ -273,15 +326,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY;  // running max (raw logit units), possibly stale
       float l = 0.f;
       for (int j = 0; j < w.n; ++j) {
+        if (lane == 0 && wq == 0) RP_TR(3 * x + 0, scnt);
         mbar_wait(&s_full[x], scnt & 1);
+        if (lane == 0 && wq == 0) RP_TR(3 * x + 1, scnt);
         ++scnt;
         tc_fence_after();
+#ifdef RP_ABL_NOSOFT
+        // ablation: no softmax work, P = stale S bits (timing only)
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&p_split[x]); mbar_arrive(&p_full[x]); }
+        if (lane == 0 && wq == 0) RP_TR(3 * x + 2, scnt - 1);
+        continue;
+#endif
         uint32_t s0[32], s1[32], s2[32], s3[32];
         tmem_ld32(trow + L::s_col(x) + 0, s0);
         tmem_ld32(trow + L::s_col(x) + 32, s1);
         tmem_ld32(trow + L::s_col(x) + 64, s2);
         tmem_ld32(trow + L::s_col(x) + 96, s3);
         tmem_wait_ld();
+        if (lane == 0 && wq == 0 && x == 0) RP_TR(10, scnt - 1);
         auto S = [&](int e) -> float {
           const uint32_t v = e < 32 ? s0[e] : e < 64 ? s1[e - 32] : e < 96 ? s2[e - 64] : s3[e - 96];
           return __uint_as_float(v);
@@ -307,44 +370,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = m_new;
           l *= alpha;
         }
-        // p = 2^(s*scale*log2e - m*scale*log2e).  Two phases so the 128
-        // exponentials (MUFU and polynomial) issue back to back, independent
-        // of each other, before any consumer touches a result: the sums and
-        // bf16 packing then run on completed values instead of stalling on
-        // MUFU latency pair by pair.
-        const float2 sc2 = make_float2(sl2, sl2);
-        const float2 ng2 = make_float2(-m * sl2, -m * sl2);
-        auto put = [&](int e, float v) {
-          const uint32_t b = __float_as_uint(v);
-          if (e < 32) s0[e] = b; else if (e < 64) s1[e - 32] = b;
-          else if (e < 96) s2[e - 64] = b; else s3[e - 96] = b;
-        };
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const float2 xv = ffma2(make_float2(S(2 * i), S(2 * i + 1)), sc2, ng2);
-          float2 pv;
-          if (kPolyMask & (1u << (i & 7))) {
-            pv = ex2_poly2(xv);
-          } else {
-            pv.x = ex2(xv.x);
-            pv.y = ex2(xv.y);
-          }
-          put(2 * i, pv.x);
-          put(2 * i + 1, pv.y);
-        }
-        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                         make_float2(0.f, 0.f)};
-        uint32_t pk[64];
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const float2 pv = make_float2(S(2 * i), S(2 * i + 1));
-          acc[i & 3] = fadd2(acc[i & 3], pv);
-          pk[i] = pack_bf16(pv.x, pv.y);
-        }
-        const float2 at = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-        l += at.x + at.y;
-        // (O_x is stable here: S_x(j) was issued after O_x += P_x(j-1) V(j-1)
-        // and its commit covers every earlier MMA.)
+        // Rescale O before any part of P is published: the P.V that follows
+        // the split arrive accumulates into O_x.  (O_x is stable here: S_x(j)
+        // was issued after O_x += P_x(j-1) V(j-1) and its commit covers every
+        // earlier MMA.)
         if (__any_sync(0xFFFFFFFFu, need)) {
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
@@ -356,13 +385,59 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st32(trow + L::o_col(x) + c * 32, o);
           }
         }
-        // P row -> TMEM columns 0..63 of S_x (bf16 pairs, A operand of P.V)
-        tmem_st32(trow + L::s_col(x), *reinterpret_cast<const uint32_t(*)[32]>(pk));
-        tmem_st32(trow + L::s_col(x) + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
+        // p = 2^(s*scale*log2e - m*scale*log2e), 32 keys per chunk: the
+        // chunk's exponentials (MUFU or polynomial on the FMA pipe) issue back
+        // to back, then the chunk is summed, packed to bf16 pairs and stored
+        // into TMEM columns [16c, 16c+16) of S_x (the A operand of P.V).
+        // After kSplitKeys keys the MMA may start P.V on them.
+        const float2 sc2 = make_float2(sl2, sl2);
+        const float2 ng2 = make_float2(-m * sl2, -m * sl2);
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        // Software pipeline over 4 chunks of 32 keys: step c issues chunk c's
+        // exponentials and, in the MUFU gaps, sums / packs / stores chunk
+        // c-1 (whose MUFU results have long retired).
+        float2 pv_prev[16];
+#pragma unroll
+        for (int c = 0; c <= 4; ++c) {
+          float2 pv_cur[16];
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (c < 4) {
+              const int e = 32 * c + 2 * i;
+              const float2 xv = ffma2v(make_float2(S(e), S(e + 1)), sc2, ng2);
+              if (kPolyMask & (1u << (i & 7))) {
+                pv_cur[i] = ex2_poly2(xv);
+              } else {
+                pv_cur[i].x = ex2v(xv.x);
+                pv_cur[i].y = ex2v(xv.y);
+              }
+            }
+            if (c > 0) {
+              acc[i & 1] = fadd2v(acc[i & 1], pv_prev[i]);
+              pk[i] = pack_bf16v(pv_prev[i].x, pv_prev[i].y);
+            }
+          }
+          if (c > 0) {
+            tmem_st16(trow + L::s_col(x) + 16 * (c - 1), pk);
+            if (32 * c == kSplitKeys) {
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&p_split[x]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
+        }
+        if (lane == 0 && wq == 0 && x == 0) RP_TR(11, scnt - 1);
+        const float2 at = fadd2(acc[0], acc[1]);
+        l += at.x + at.y;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[x]);
+        if (lane == 0 && wq == 0) RP_TR(3 * x + 2, scnt - 1);
       }
       // epilogue: wait for the unit's last P.V, O / l -> bf16 -> global
       mbar_wait(&o_done[x], ucnt & 1);

@@ -165,6 +165,11 @@ extern "C" {
 const char* rp_last_error(void) { return t_err.c_str(); }
 const char* rp_version(void) { return "dynrad-b200 0.1 (sm_100a)"; }
 int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
+#ifdef RP_TRACE
+int rp_debug_trace(void* host) {
+  return cudaMemcpyFromSymbol(host, attn::g_trace, sizeof(attn::g_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 rp_status rp_make_grid(int nf, int nt, int bs, rp_grid* out) {
   return guarded([&] {

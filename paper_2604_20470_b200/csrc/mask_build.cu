@@ -93,7 +93,16 @@ __global__ void fy_link_kernel(const uint64_t* __restrict__ keys, int64_t total,
   }
 }
 
-// Value swapped into slot d at step d, then counted into its tile column.
+// Value swapped into slot d at step d: the target r_d itself when no
+// earlier step touched it, else A(e) chased down the tlast links.
+RP_DEV int64_t fy_slot_value(const DJob& jb, int64_t d, int32_t p, const int32_t* tl) {
+  if (p < 0) return fy_target(jb, d);  // slot r_d untouched before step d
+  int64_t e = p;  // A(e): value at slot e before step e
+  while (tl[e] >= 0) e = tl[e];
+  return e;
+}
+
+// ... then counted into its tile column (build_mask).
 __global__ void fy_count_kernel(const DJob* __restrict__ jobs, const int* __restrict__ batch_jobs,
                                 const int64_t* __restrict__ off, int n_jobs, int64_t total,
                                 const int32_t* __restrict__ prev,
@@ -104,20 +113,160 @@ __global__ void fy_count_kernel(const DJob* __restrict__ jobs, const int* __rest
   const int lj = find_job(off, n_jobs, x);
   const DJob& jb = jobs[batch_jobs[lj]];
   const int64_t d = x - off[lj];
-  const int32_t* tl = tlast + off[lj];
-  int64_t val;
-  const int32_t p = prev[x];
-  if (p < 0) {
-    val = fy_target(jb, d);  // slot r_d untouched before step d
-  } else {
-    // A(e): value at slot e before step e = A(tlast[e]) chased down.
-    int64_t e = p;
-    while (tl[e] >= 0) e = tl[e];
-    val = e;
-  }
+  const int64_t val = fy_slot_value(jb, d, prev[x], tlast + off[lj]);
   int64_t u, v;
   band_uv(val, nt, jb.width, &u, &v);
   add_count(jb, counts, nt, bs, u, v);
+}
+
+// ... or emitted as the (u, v) of slot d (static_select, one job).
+__global__ void fy_value_kernel(const DJob* __restrict__ job, int64_t k,
+                                const int32_t* __restrict__ prev,
+                                const int32_t* __restrict__ tlast, int64_t nt,
+                                int64_t* __restrict__ uv) {
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d >= k) return;
+  const int64_t val = fy_slot_value(*job, d, prev[d], tlast);
+  band_uv(val, nt, job->width, &uv[2 * d], &uv[2 * d + 1]);
+}
+
+// ---------------------------------- per-frame-pair selection operators -----
+// normalize_scores' z (selection.cpp:144-146) from the pinned stats.
+__global__ void zscore_kernel(const float* __restrict__ s, int64_t n,
+                              const double2* __restrict__ st, double* __restrict__ z) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n) z[x] = zscore(s[x], *st);
+}
+
+// dynamic_select keep set (selection.cpp:159-161), in flat order: per-CTA
+// counts, then an ordered scatter after a host-side exclusive scan.
+constexpr int kSelTile = 1024;
+__global__ void keep_count_kernel(const double* __restrict__ z, int64_t n, double tau,
+                                  int32_t* __restrict__ cta_count) {
+  __shared__ int32_t c;
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * kSelTile + threadIdx.x;
+  int mine = 0;
+  for (int64_t y = x; y < n && y < (static_cast<int64_t>(blockIdx.x) + 1) * kSelTile;
+       y += blockDim.x)
+    mine += z[y] >= tau;
+  if (mine) atomicAdd(&c, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) cta_count[blockIdx.x] = c;
+}
+__global__ void keep_scatter_kernel(const double* __restrict__ z, int64_t n, double tau,
+                                    const int64_t* __restrict__ cta_off, int64_t nt, int64_t w,
+                                    int64_t* __restrict__ uv) {
+  // one warp-ordered pass per CTA tile keeps the flat order
+  __shared__ int32_t base;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kSelTile;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t y0 = t0; y0 < n && y0 < t0 + kSelTile; y0 += blockDim.x) {
+    const int64_t y = y0 + threadIdx.x;
+    const bool keep = y < n && y < t0 + kSelTile && z[y] >= tau;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+    __shared__ int32_t warp_tot[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) warp_tot[wid] = __popc(m);
+    __syncthreads();
+    int before = base;
+    for (int q = 0; q < wid; ++q) before += warp_tot[q];
+    if (keep) {
+      const int64_t slot = cta_off[blockIdx.x] + before + __popc(m & ((1u << lane) - 1));
+      band_uv(y, nt, w, &uv[2 * slot], &uv[2 * slot + 1]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) tot += warp_tot[q];
+      base += tot;
+    }
+    __syncthreads();
+  }
+}
+// Fallback (selection.cpp:163-175): the fallback_k best z, ties to the lower
+// flat index, emitted in ascending flat order.  One CTA, k argmax rounds.
+__global__ void fallback_pick_kernel(const double* __restrict__ z, int64_t n, int k, int64_t nt,
+                                     int64_t w, int64_t* __restrict__ uv) {
+  __shared__ double bz[32];
+  __shared__ int64_t bi[32];
+  __shared__ int64_t last_pick;
+  __shared__ double last_z;
+  if (threadIdx.x == 0) {
+    last_pick = -1;
+    last_z = INFINITY;
+  }
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    double best = -INFINITY;
+    int64_t besti = -1;
+    for (int64_t x = threadIdx.x; x < n; x += blockDim.x) {
+      const double zz = z[x];
+      if (!(zz < last_z || (zz == last_z && x > last_pick))) continue;
+      if (besti < 0 || zz > best || (zz == best && x < besti)) {
+        best = zz;
+        besti = x;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oz = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xFFFFFFFFu, besti, o);
+      if (oi >= 0 && (besti < 0 || oz > best || (oz == best && oi < besti))) {
+        best = oz;
+        besti = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      bz[threadIdx.x >> 5] = best;
+      bi[threadIdx.x >> 5] = besti;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < static_cast<int>(blockDim.x >> 5); ++q)
+        if (bi[q] >= 0 && (bi[0] < 0 || bz[q] > bz[0] || (bz[q] == bz[0] && bi[q] < bi[0]))) {
+          bz[0] = bz[q];
+          bi[0] = bi[q];
+        }
+      uv[2 * round] = bi[0];  // flat index; converted below
+      last_pick = bi[0];
+      last_z = bz[0];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int a = 1; a < k; ++a)  // ascending flat order (selection.cpp:174)
+      for (int b = a; b > 0 && uv[2 * (b - 1)] > uv[2 * b]; --b) {
+        const int64_t t = uv[2 * b];
+        uv[2 * b] = uv[2 * (b - 1)];
+        uv[2 * (b - 1)] = t;
+      }
+    for (int a = 0; a < k; ++a) {
+      const int64_t flat = uv[2 * a];
+      band_uv(flat, nt, w, &uv[2 * a], &uv[2 * a + 1]);
+    }
+  }
+}
+
+// Token mask (S' x S' bits) -> block mask at block size B: the block bit is
+// its top-left token bit; `bad` counts blocks that are not uniform.
+__global__ void token_to_block_kernel(const uint8_t* __restrict__ tok, int64_t dim,
+                                      int64_t trb, int bs, int64_t nb, int64_t brb,
+                                      uint32_t* __restrict__ words,
+                                      unsigned long long* __restrict__ bad) {
+  const int64_t blk = blockIdx.x;  // block row * nb + block col
+  const int64_t br = blk / nb, bc = blk % nb;
+  const auto bit = [&](int64_t r, int64_t c) { return (tok[r * trb + c / 8] >> (c % 8)) & 1; };
+  const int ref = bit(br * bs, bc * bs);
+  int diff = 0;
+  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(bs) * bs; e += blockDim.x)
+    diff |= bit(br * bs + e / bs, bc * bs + e % bs) != ref;
+  diff = __syncthreads_or(diff);
+  if (threadIdx.x == 0) {
+    if (diff) atomicAdd(bad, 1ull);
+    if (ref) set_block(words, brb, br, bc);
+  }
 }
 
 // ------------------------------------ K2/K3 exact engine (fp64 SIMT) -------
@@ -709,6 +858,214 @@ rp_status rp_build_mask(const rp_grid* g, const rp_config* c, uint64_t seed,
   }
   rp_plan_destroy(p);
   return r;
+}
+
+// ------------------------------------------------ selection operators ------
+namespace {
+
+int64_t band_count(const rp_band* b) {
+  if (!b) throw std::invalid_argument("band: null");
+  if (b->tokens_per_frame < 1 || b->width < 0)
+    throw std::invalid_argument("band: bad geometry");
+  return b->retained ? plan::band_pairs(b->tokens_per_frame, b->width) : 0;
+}
+
+}  // namespace
+
+rp_status rp_static_select(const rp_band* band, double ratio, uint64_t seed, int64_t* uv_dev,
+                           int64_t cap, int64_t* count, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (!count) throw std::invalid_argument("static_select: null count");
+    const int64_t n = band_count(band);
+    *count = 0;
+    if (n == 0) return;
+    if (!(ratio > 0.0 && ratio <= 1.0))
+      throw std::invalid_argument("static_select: ratio must be in (0, 1]");
+    int64_t k = static_cast<int64_t>(std::floor(static_cast<double>(n) * ratio));
+    if (k < 1) k = 1;
+    if (k > cap || !uv_dev) throw std::out_of_range("static_select: output capacity");
+    if (n > (int64_t{1} << 31)) throw std::out_of_range("static_select: band too large");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    DJob jb{};
+    jb.i = band->frame_i;
+    jb.j = band->frame_j;
+    jb.width = band->width;
+    jb.n = n;
+    jb.k = k;
+    jb.seed = pair_seed(seed, band->frame_i, band->frame_j);
+    const int bits = std::max(1, bit_length(static_cast<uint64_t>(n - 1)));
+    DevBuf<DJob> d_job(1, s);
+    d_job.upload(&jb, 1);
+    const int zero = 0;
+    DevBuf<int> d_batch(1, s);
+    d_batch.upload(&zero, 1);
+    const int64_t off[2] = {0, k};
+    DevBuf<int64_t> d_off(2, s);
+    d_off.upload(off, 2);
+    DevBuf<uint64_t> keys(k, s), sorted(k, s);
+    DevBuf<int32_t> prev(k, s), tlast(k, s);
+    RP_CUDA(cudaMemsetAsync(tlast.p, 0xFF, sizeof(int32_t) * k, s));
+    const unsigned grid = static_cast<unsigned>((k + 255) / 256);
+    fy_draw_kernel<<<grid, 256, 0, s>>>(d_job.p, d_batch.p, d_off.p, 1, k, bits, keys.p);
+    RP_LAUNCHED();
+    size_t tmp_bytes = 0;
+    RP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, k, 0,
+                                           2 * bits + 1, s));
+    DevBuf<uint8_t> tmp(tmp_bytes, s);
+    RP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, k, 0,
+                                           2 * bits + 1, s));
+    count_launch();
+    fy_link_kernel<<<grid, 256, 0, s>>>(sorted.p, k, bits, d_off.p, prev.p, tlast.p, d_job.p,
+                                        d_batch.p);
+    RP_LAUNCHED();
+    fy_value_kernel<<<grid, 256, 0, s>>>(d_job.p, k, prev.p, tlast.p, band->tokens_per_frame,
+                                         uv_dev);
+    RP_LAUNCHED();
+    RP_CUDA(cudaStreamSynchronize(s));
+    *count = k;
+  });
+}
+
+rp_status rp_proxy_scores(const rp_tensor* q, const rp_tensor* k, int n_heads,
+                          const rp_band* band, float* scores_dev, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (n_heads < 1) throw std::invalid_argument("proxy_scores: batch has no heads");
+    if (!q || !k || !q->data || !k->data || q->heads < n_heads || k->heads < n_heads ||
+        q->head_dim != k->head_dim || q->dtype != k->dtype)
+      throw std::invalid_argument("feature batch: queries/keys shape mismatch");
+    const int64_t n = band_count(band);
+    const int64_t nt = band->tokens_per_frame;
+    const int64_t qi = static_cast<int64_t>(band->frame_i) * nt;
+    const int64_t kj = static_cast<int64_t>(band->frame_j) * nt;
+    if (band->frame_i < 0 || band->frame_j < 0 || qi + nt > q->tokens || kj + nt > k->tokens)
+      throw std::out_of_range("proxy_scores: frame outside feature batch");
+    if (n == 0) return;
+    if (!scores_dev) throw std::invalid_argument("proxy_scores: null output");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    DJob jb{};
+    jb.i = band->frame_i;
+    jb.j = band->frame_j;
+    jb.width = band->width;
+    jb.n = n;
+    DevBuf<DJob> d_job(1, s);
+    d_job.upload(&jb, 1);
+    const int zero = 0;
+    DevBuf<int> d_batch(1, s);
+    d_batch.upload(&zero, 1);
+    const int64_t off[2] = {0, n};
+    DevBuf<int64_t> d_off(2, s);
+    d_off.upload(off, 2);
+    const Feat f = make_feat(q, k, n_heads);
+    exact_scores_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        d_job.p, d_batch.p, d_off.p, 1, n, f, nt, scores_dev);
+    RP_LAUNCHED();
+    RP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+rp_status rp_normalize_scores(const float* scores_dev, int64_t n, double* z_dev, double* mean,
+                              double* stddev, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (n < 0) throw std::invalid_argument("normalize_scores: negative count");
+    if (n == 0) {
+      if (mean) *mean = 0.0;
+      if (stddev) *stddev = 0.0;
+      return;
+    }
+    if (!scores_dev || !z_dev) throw std::invalid_argument("normalize_scores: null buffer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t off[2] = {0, n};
+    DevBuf<int64_t> d_off(2, s);
+    d_off.upload(off, 2);
+    DevBuf<double2> st(1, s);
+    seq_stats_kernel<<<1, 32, 0, s>>>(d_off.p, 1, scores_dev, st.p);
+    RP_LAUNCHED();
+    zscore_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(scores_dev, n, st.p,
+                                                                          z_dev);
+    RP_LAUNCHED();
+    double2 h;
+    RP_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    if (mean) *mean = h.x;
+    if (stddev) *stddev = h.y;
+  });
+}
+
+rp_status rp_dynamic_select(const rp_band* band, const double* z_dev, int64_t n,
+                            double threshold, int fallback_k, int64_t* uv_dev, int64_t cap,
+                            int64_t* count, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (!count) throw std::invalid_argument("dynamic_select: null count");
+    const int64_t pc = band_count(band);
+    if (n != pc) throw std::invalid_argument("dynamic_select: score count mismatch");
+    *count = 0;
+    if (n == 0) return;
+    if (!z_dev || !uv_dev) throw std::invalid_argument("dynamic_select: null buffer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t tiles = (n + kSelTile - 1) / kSelTile;
+    DevBuf<int32_t> cnt(tiles, s);
+    keep_count_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(z_dev, n, threshold, cnt.p);
+    RP_LAUNCHED();
+    std::vector<int32_t> hc(tiles);
+    RP_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, sizeof(int32_t) * tiles, cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> off(tiles);
+    int64_t kept = 0;
+    for (int64_t t = 0; t < tiles; ++t) {
+      off[t] = kept;
+      kept += hc[t];
+    }
+    if (kept > 0) {
+      if (kept > cap) throw std::out_of_range("dynamic_select: output capacity");
+      DevBuf<int64_t> d_off(tiles, s);
+      d_off.upload(off.data(), tiles);
+      keep_scatter_kernel<<<static_cast<unsigned>(tiles), 256, 0, s>>>(
+          z_dev, n, threshold, d_off.p, band->tokens_per_frame, band->width, uv_dev);
+      RP_LAUNCHED();
+      RP_CUDA(cudaStreamSynchronize(s));
+      *count = kept;
+      return;
+    }
+    const int64_t k = std::min<int64_t>(std::max(fallback_k, 0), n);
+    if (k > cap) throw std::out_of_range("dynamic_select: output capacity");
+    if (k > 0) {
+      fallback_pick_kernel<<<1, 1024, 0, s>>>(z_dev, n, static_cast<int>(k),
+                                              band->tokens_per_frame, band->width, uv_dev);
+      RP_LAUNCHED();
+      RP_CUDA(cudaStreamSynchronize(s));
+    }
+    *count = k;
+  });
+}
+
+rp_status rp_token_mask_to_blocks(const uint8_t* token_bits_dev, int64_t dim, int block_size,
+                                  uint8_t* block_bits_dev, int* uniform, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (block_size < 1 || dim < 1 || dim % block_size)
+      throw std::invalid_argument("token mask: block size must divide the mask dimension");
+    if (!token_bits_dev || !block_bits_dev) throw std::invalid_argument("token mask: null buffer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nb = dim / block_size, brb = (nb + 7) / 8;
+    const size_t words = static_cast<size_t>((nb * brb + 3) / 4);
+    DevBuf<uint32_t> w(words, s);
+    DevBuf<unsigned long long> bad(1, s);
+    RP_CUDA(cudaMemsetAsync(w.p, 0, words * 4, s));
+    RP_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+    token_to_block_kernel<<<static_cast<unsigned>(nb * nb), 256, 0, s>>>(
+        token_bits_dev, dim, (dim + 7) / 8, block_size, nb, brb, w.p, bad.p);
+    RP_LAUNCHED();
+    RP_CUDA(cudaMemcpyAsync(block_bits_dev, w.p, static_cast<size_t>(nb * brb),
+                            cudaMemcpyDeviceToDevice, s));
+    unsigned long long h = 0;
+    RP_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    if (uniform) *uniform = h == 0;
+  });
 }
 
 }  // extern "C"

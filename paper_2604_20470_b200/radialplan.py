@@ -328,6 +328,70 @@ def aggregate_block(kept_in_tile, col_threshold: float, mask_threshold: float,
     return active / block_size >= mask_threshold
 
 
+# ------------------------------------ per-frame-pair selection operators ---
+# selection.hpp:60-82, each on its own CUDA kernel (rp_static_select, ...).
+def _band(cands: CandidateSet, tokens_per_frame: Optional[int] = None) -> L.Band:
+    return L.Band(int(cands.frame_i), int(cands.frame_j),
+                  int(tokens_per_frame or cands.tokens_per_frame), int(cands.width),
+                  1 if cands.retained else 0)
+
+
+def static_select(cands: CandidateSet, ratio: float, seed: int):
+    """selection.cpp:61-91 -> list of (u, v) in Fisher-Yates slot order."""
+    torch = _torch()
+    n = cands.pair_count()
+    cap = max(1, n)
+    uv = torch.empty((cap, 2), dtype=torch.int64, device="cuda")
+    k = C.c_int64(0)
+    b = _band(cands)
+    L.check(L.lib().rp_static_select(C.byref(b), float(ratio), int(seed) & (2**64 - 1),
+                                     C.c_void_p(uv.data_ptr()), cap, C.byref(k), None))
+    return [tuple(x) for x in uv[: k.value].cpu().tolist()]
+
+
+def proxy_scores(features: "FeatureBatch", frame_i: int, frame_j: int, cands: CandidateSet,
+                 tokens_per_frame: int):
+    """selection.cpp:93-123 on device features [tokens, heads, d] -> float32 scores."""
+    torch = _torch()
+    q, k = features.queries, features.keys
+    n = cands.pair_count()
+    out = torch.empty(max(n, 1), dtype=torch.float32, device="cuda")
+    tq, tk = _tensor(q), _tensor(k)
+    b = _band(cands, tokens_per_frame)
+    b.frame_i, b.frame_j = int(frame_i), int(frame_j)
+    L.check(L.lib().rp_proxy_scores(C.byref(tq), C.byref(tk), int(q.shape[1]), C.byref(b),
+                                    C.c_void_p(out.data_ptr()), None))
+    return out[:n]
+
+
+def normalize_scores(scores, stats: Optional[dict] = None):
+    """selection.cpp:125-148: device float32 scores -> float64 z (+ mean/stddev)."""
+    torch = _torch()
+    n = int(scores.numel())
+    z = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    mean, sd = C.c_double(0.0), C.c_double(0.0)
+    L.check(L.lib().rp_normalize_scores(C.c_void_p(scores.data_ptr()) if n else None, n,
+                                        C.c_void_p(z.data_ptr()), C.byref(mean), C.byref(sd),
+                                        None))
+    if stats is not None:
+        stats["mean"], stats["stddev"] = mean.value, sd.value
+    return z[:n]
+
+
+def dynamic_select(cands: CandidateSet, normalized, threshold: float, fallback_k: int = 1):
+    """selection.cpp:150-185: device float64 z -> list of (u, v)."""
+    torch = _torch()
+    n = int(normalized.numel())
+    cap = max(1, n)
+    uv = torch.empty((cap, 2), dtype=torch.int64, device="cuda")
+    k = C.c_int64(0)
+    b = _band(cands)
+    L.check(L.lib().rp_dynamic_select(C.byref(b), C.c_void_p(normalized.data_ptr()), n,
+                                      float(threshold), int(fallback_k),
+                                      C.c_void_p(uv.data_ptr()), cap, C.byref(k), None))
+    return [tuple(x) for x in uv[: k.value].cpu().tolist()]
+
+
 # ------------------------------------------------------------- devices ----
 def _tensor(t, dtype_code=None) -> L.Tensor:
     """Describe a torch CUDA tensor [tokens, heads, head_dim] (head_dim contiguous)."""
