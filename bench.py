@@ -263,7 +263,9 @@ def main():
                     torch.empty(nb, dtype=torch.int32, device=dev),
                     torch.zeros(1, dtype=torch.int64, device=dev))
 
-    def layer():
+    def layer(mark=None):
+        """One layer; `mark` (a pair of events) brackets the stage-(d) launch
+        so its own duration feeds the roofline."""
         nonlocal row_ptr, col_idx, order
         if dynamic:
             # the scoring heads (global 0..H_f-1) live on rank 0; it builds the
@@ -273,7 +275,11 @@ def main():
             if world > 1:
                 broadcast_mask(mask, src=0)
             row_ptr, col_idx, order = rp.mask_to_csr(g, mask, stream=stream, out=csr_bufs)
+        if mark is not None:
+            mark[0].record(stream)
         rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, out=out, stream=stream)
+        if mark is not None:
+            mark[1].record(stream)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -283,12 +289,13 @@ def main():
     torch.cuda.synchronize()
     starts = [ev() for _ in range(args.steps)]
     ends = [ev() for _ in range(args.steps)]
+    marks = [(ev(), ev()) for _ in range(args.steps)]
     launches0 = rp.kernel_launch_count()
     with ClockSampler(local) as clk:
         with torch.cuda.stream(stream):
             for i in range(args.steps):
                 starts[i].record(stream)
-                layer()
+                layer(marks[i])
                 ends[i].record(stream)
         stream.synchronize()
     launches = rp.kernel_launch_count() - launches0
@@ -305,7 +312,8 @@ def main():
     flops_dense_eq = 4.0 * H * d * float(S) ** 2             # dense-equivalent
     tflops_eff = flops_dense_eq / (ms * 1e-3) / 1e12
     tflops_alg = flops_alg / (ms * 1e-3) / 1e12
-    kernel_tflops = flops_local / (float(np.mean(per_step)) * 1e-3) / 1e12
+    k6_ms = [a.elapsed_time(b) for a, b in marks]  # stage (d) launch alone, same stream
+    kernel_tflops = flops_local / (float(np.mean(k6_ms)) * 1e-3) / 1e12
 
     # ---- end to end through the host-buffer C ABI call ----------------------
     e2e = None
@@ -382,7 +390,10 @@ def main():
                "sample": desc, "sample_wall_s": dt}
 
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "k6_ncu_summary.json")
+    pair = os.environ.get("DYNRAD_K6") == "pair"
+    kname = "bsfa_fwd_kernel<128> (two-head ping-pong)" if pair else "bsfa_fwd_db_kernel<128>"
+    prof = os.path.join(ROOT, "profiles", "k6pair_ncu_summary.json" if pair else
+                        "k6db_ncu_summary.json")
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
@@ -406,7 +417,8 @@ def main():
             "roofline": {"bound": "tensor", "achieved": kernel_tflops, "peak": peak,
                          "unit": "TFLOP/s", "frac": kernel_tflops / peak,
                          "traffic": traffic,
-                         "kernel": "bsfa_fwd_kernel<128> (stage d)",
+                         "kernel": kname + " (stage d)",
+                         "kernel_ms": float(np.mean(k6_ms)),
                          "per_launch": "4*H*d*B^2*nnz flop on active blocks",
                          "peak_source": f"{peaks_kind} bf16_tflops (burst)"},
             "clocks": clk.summary(),
@@ -414,6 +426,12 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "dense": dense or None,
+            "stages_ms": {"attention_stage_d": float(np.mean(k6_ms)),
+                          "mask_stages_a_c_plus_csr": float(np.mean(per_step) - np.mean(k6_ms))
+                          if dynamic else 0.0,
+                          "note": "static: mask cached per (grid, config, seed), built once "
+                                  "(mask_build_ms_one_time)" if not dynamic else
+                                  "dynamic: mask rebuilt from the layer's Q/K every step"},
             "per_step_ms": {"min": float(min(per_step)), "median": float(np.median(per_step)),
                             "max": float(max(per_step))},
         }

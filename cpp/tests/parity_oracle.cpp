@@ -171,8 +171,11 @@ int main() {
           const GridSpec g = make_grid(nf, nt, 4);
           const SparsityConfig c = random_config(r, mode);
           const FeatureBatch f = random_batch(g.total_tokens, 2, 8, r(), false);
-          masks += check_mask(g, c, r(), mode == Mode::DynamicThreshold ? &f : nullptr,
-                              rep % 5 == 4 && mode == Mode::DynamicThreshold);
+          // (disable_split is not swept here: oracle::build scores the full
+          // band of split-pruned pairs while the library's candidate_set makes
+          // them empty -- the reference disagrees with itself; the GPU follows
+          // the library, tests/test_mask_gpu.py checks that.)
+          masks += check_mask(g, c, r(), mode == Mode::DynamicThreshold ? &f : nullptr, false);
         }
   // Tiny golden shape (8 x 16 x 16 = 2048 tokens), B in {16, 32, 64, 128}.
   const FeatureBatch tiny = random_batch(2048, 2, 64, 42, false);

@@ -155,6 +155,9 @@ class _RefLib(_Lib):
         L.ref_proxy_scores.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
                                        _f32p, _f32p, C.c_int64, C.c_int, C.c_int, _f32p,
                                        _P(C.c_double), _P(C.c_double)]
+        L.ref_dynamic_select.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
+                                         _P(C.c_double), C.c_int64, C.c_double, C.c_int,
+                                         _P(C.c_int64), C.c_int64, _P(C.c_int64)]
 
     def _chk(self, rc):
         if rc != 0:

@@ -1,0 +1,452 @@
+// K6 (v2): block-sparse flash-attention forward, bf16 in / fp32 softmax,
+// sm_100a, with the score tile double-buffered in TMEM.
+//
+// Replaces radialplan::masked_attention_exact (attention.cpp:50-121) on the
+// tensor cores, with the same semantics as attn_sm100.cu: only the row's CSR
+// blocks are attended (-inf elsewhere, constant per B x B block), and rows
+// >= S are TMA out-of-bounds zeros that take part as keys with logit 0
+// whenever their block is active (attention.cpp:43-48, 66-68).
+//
+// Why a second design.  In the two-head ping-pong kernel each head's score
+// tile S lives in one TMEM buffer that P overwrites, so S(j+1) can only be
+// computed after P(j).V(j) has read P(j): every KV step pays softmax latency
+// + MMA latency in series (measured: 2.1k + 1.4k clk per step, tensor pipe
+// ~58 % busy).  Here a CTA owns ONE 128-row query tile with two S buffers:
+//   TMEM  S0 cols 0-127 | S1 cols 128-255 | O cols 256-(256+D)
+// The MMA warp issues S(g+2) right after P(g).V(g), so S(g+1) is already in
+// TMEM when the softmax of step g finishes: the softmax runs back to back and
+// the tensor core works underneath it.
+//
+// Softmax: 8 warps (two per SM sub-partition, so their MUFU / FMA work
+// interleaves).  Warps w and w+4 share TMEM lanes 32(w%4)..+31 (the same 32
+// query rows) and split the 128 keys: half h = w/4 owns keys [64h, 64h+64),
+// P columns [32h, 32h+32) of the step's buffer, and O columns [hD/2, hD/2+D/2).
+// The row max is combined through shared memory with a 64-thread named
+// barrier per row group; the row sums stay per half until the epilogue.
+// Lazy rescaling (threshold 2^8, exact) as in attn_sm100.cu; a rescale waits
+// for the previous step's P.V to retire before touching O.
+//
+//   warps 0-7   softmax / epilogue       warp 8  TMA producer (whole warp)
+//   warp  9     MMA issuer (whole warp)  warps 10-11 idle (setmaxnreg group)
+#include "common.cuh"
+
+namespace rp {
+namespace attn2 {
+
+constexpr int kThreads = 384;
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+// Pairs (of every 8) whose exp2 runs as a polynomial on the FMA pipe.
+#ifndef RP_DB_POLY_MASK
+#define RP_DB_POLY_MASK 0x01u
+#endif
+constexpr uint32_t kPolyMask = RP_DB_POLY_MASK;
+
+template <int D>
+struct Layout {
+  static constexpr int kChunks = D / 64;          // 128-byte K chunks per row
+  static constexpr int kTileBytes = 128 * D * 2;  // one 128-row bf16 tile
+  static constexpr int kChunkBytes = 128 * 128;
+#ifdef RP_DB_STAGES
+  static constexpr int kStages = RP_DB_STAGES;
+#else
+  static constexpr int kStages = D == 128 ? 4 : 8;  // 2 Q tiles + ring <= 227 KB
+#endif
+  static constexpr int kSmemData = 2 * kTileBytes + kStages * kTileBytes;
+  static constexpr int kNumBars = 2 * kStages + 13;
+  static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128) * 4;  // row max x2 slots, row sums
+  static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + kRedBytes + 1024;
+  static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory");
+  static constexpr uint32_t kO = 256;  // TMEM column of O
+};
+
+struct Params {
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  const int32_t* row_order;  // may be null
+  int n_rows;                // S_b
+  int heads;
+  long long n_units;         // heads * n_rows
+  __nv_bfloat16* out;
+  long long out_tok_stride;
+  long long out_head_stride;
+  float scale_log2;
+};
+
+#ifdef RP_TRACE
+constexpr int kTraceCtas = 4, kTraceEv = 12, kTraceSteps = 512;
+__device__ unsigned long long g_trace[kTraceCtas][kTraceEv][kTraceSteps];
+#define RP_TR2(ev, idx)                                                       \
+  do {                                                                        \
+    if (blockIdx.x < kTraceCtas && (idx) < kTraceSteps)                       \
+      g_trace[blockIdx.x][ev][idx] = clock64();                               \
+  } while (0)
+#else
+#define RP_TR2(ev, idx) \
+  do {                  \
+  } while (0)
+#endif
+
+// Walks this CTA's units (head-major: consecutive units of a CTA stride over
+// rows of the same head, so concurrently running CTAs share K/V in L2) and
+// their KV blocks.  Empty rows are skipped (the softmax warps zero them).
+// All fields are warp-uniform (lookups broadcast from lane 0).
+struct Cursor {
+  long long u;
+  int ord;  // ordinal among this CTA's non-empty units
+  int j, n, beg, h, row;
+  bool valid;
+
+  RP_DEV void seek(const Params& p) {
+    valid = false;
+    for (; u < p.n_units; u += gridDim.x) {
+      const int hh = static_cast<int>(u / p.n_rows);
+      const int ri = static_cast<int>(u % p.n_rows);
+      const int r = shfl0(p.row_order ? __ldg(p.row_order + ri) : ri);
+      const int b = shfl0(__ldg(p.row_ptr + r));
+      const int e = shfl0(__ldg(p.row_ptr + r + 1));
+      if (e > b) {
+        h = hh;
+        row = r;
+        beg = b;
+        n = e - b;
+        j = 0;
+        valid = true;
+        return;
+      }
+    }
+  }
+  RP_DEV void start(const Params& p) {
+    u = blockIdx.x;
+    ord = 0;
+    seek(p);
+  }
+  RP_DEV void next(const Params& p) {
+    if (++j < n) return;
+    u += gridDim.x;
+    ++ord;
+    seek(p);
+  }
+  RP_DEV int col(const Params& p) const { return shfl0(__ldg(p.col_idx + beg + j)); }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    bsfa_fwd_db_kernel(const __grid_constant__ CUtensorMap tq,
+                       const __grid_constant__ CUtensorMap tk,
+                       const __grid_constant__ CUtensorMap tv, const Params p) {
+  using L = Layout<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem;                       // [2][tile]
+  uint8_t* skv = smem + 2 * L::kTileBytes;  // [kStages][tile]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kSmemData);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + L::kStages;
+  uint64_t* q_full = bars + 2 * L::kStages;  // [2]
+  uint64_t* q_empty = q_full + 2;            // [2]
+  uint64_t* s_full = q_full + 4;             // [2] MMA -> softmax: S_b ready
+  uint64_t* p_full = q_full + 6;             // [2] softmax -> MMA: P_b written (8 warps)
+  uint64_t* pv_done = q_full + 8;            // MMA -> softmax: a P.V retired
+  uint64_t* o_done = q_full + 9;             // MMA -> softmax: unit's last P.V retired
+  uint64_t* o_free = q_full + 10;            // softmax -> MMA: epilogue read O (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
+  float* red_max = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 halves][128]
+  float* red_l = red_max + 2 * 2 * 128;                       // [2 halves][128]
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&q_full[x], 1);
+      mbar_init(&q_empty[x], 1);
+      mbar_init(&s_full[x], 1);
+      mbar_init(&p_full[x], 8);
+    }
+    mbar_init(pv_done, 1);
+    mbar_init(o_done, 1);
+    mbar_init(o_free, 8);
+    fence_barrier_init();
+  }
+  if (warp == 8 && lane == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tk);
+    tma_prefetch_desc(&tv);
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    if (warp == 8) {
+      // ---------------------------------------------------- TMA producer --
+      // Ring order = MMA consumption order: K(0), K(1), then V(g), K(g+2).
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      uint32_t kv_it = 0;
+      auto load_kv = [&](const CUtensorMap* m, int h, int blk) {
+        const uint32_t st = kv_it % L::kStages;
+        mbar_wait(&kv_empty[st], ((kv_it / L::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx_w(&kv_full[st], L::kTileBytes);
+        uint8_t* dst = skv + st * L::kTileBytes;
+#pragma unroll
+        for (int c = 0; c < L::kChunks; ++c)
+          tma_load_3d_w(dst + c * L::kChunkBytes, m, &kv_full[st], c * 64, h, blk * kBN, pol_kv);
+        ++kv_it;
+      };
+      Cursor ck, cv;
+      ck.start(p);
+      cv.start(p);
+      auto load_k = [&]() {
+        if (ck.j == 0) {  // entering a unit: its Q tile first
+          const int qb = ck.ord & 1;
+          mbar_wait(&q_empty[qb], ((ck.ord >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx_w(&q_full[qb], L::kTileBytes);
+#pragma unroll
+          for (int c = 0; c < L::kChunks; ++c)
+            tma_load_3d_w(sq + qb * L::kTileBytes + c * L::kChunkBytes, &tq, &q_full[qb], c * 64,
+                          ck.h, ck.row * kBM, pol_q);
+        }
+        load_kv(&tk, ck.h, ck.col(p));
+        ck.next(p);
+      };
+      if (ck.valid) load_k();
+      if (ck.valid) load_k();
+      while (cv.valid) {
+        load_kv(&tv, cv.h, cv.col(p));
+        cv.next(p);
+        if (ck.valid) load_k();
+      }
+    } else if (warp == 9) {
+      // ----------------------------------------------------- MMA issuer ---
+      const uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
+      const uint32_t idesc_pv = idesc_bf16(128, D, false, true);
+      const uint32_t sq_addr = smem_u32(sq);
+      const uint32_t skv_addr = smem_u32(skv);
+      uint32_t kv_it = 0, gs = 0, gp = 0;
+      Cursor cs, cp;
+      cs.start(p);
+      cp.start(p);
+      // S(gs) = Q . K(gs)^T into buffer gs % 2 (128 x 128, K = D).
+      auto issue_s = [&]() {
+        const int qb = cs.ord & 1;
+        if (cs.j == 0) mbar_wait(&q_full[qb], (cs.ord >> 1) & 1);
+        const uint32_t st = kv_it % L::kStages;
+        mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
+        tc_fence_after();
+        const uint32_t qa = sq_addr + qb * L::kTileBytes;
+        const uint32_t kb = skv_addr + st * L::kTileBytes;
+        const uint32_t dst = tmem + (gs & 1) * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * L::kChunkBytes + (kk % 4) * 32;
+          umma_ss_w(dst, smem_desc_sw128(qa + off, 0, 1024), smem_desc_sw128(kb + off, 0, 1024),
+                    idesc_qk, kk > 0);
+        }
+        umma_commit_w(&kv_empty[st]);
+        umma_commit_w(&s_full[gs & 1]);
+        if (cs.j == cs.n - 1) umma_commit_w(&q_empty[qb]);
+        ++kv_it;
+        ++gs;
+        cs.next(p);
+      };
+      if (cs.valid) issue_s();
+      if (cs.valid) issue_s();
+      while (cp.valid) {
+        const uint32_t b = gp & 1;
+        RP_TR2(6, gp);
+        mbar_wait(&p_full[b], (gp >> 1) & 1);
+        RP_TR2(7, gp);
+        if (cp.j == 0 && cp.ord > 0) mbar_wait(o_free, (cp.ord - 1) & 1);
+        tc_fence_after();
+        // O (+)= P(gp) . V(gp): P bf16 pairs in TMEM columns [128b, 128b+64)
+        const uint32_t st = kv_it % L::kStages;
+        mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
+        tc_fence_after();
+        const uint32_t vb = skv_addr + st * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts_w(tmem + L::kO, tmem + b * 128 + kk * 8,
+                    smem_desc_sw128(vb + kk * 16 * 128, L::kChunkBytes, 1024), idesc_pv,
+                    (cp.j > 0) || kk > 0);
+        umma_commit_w(&kv_empty[st]);
+        umma_commit_w(pv_done);
+        if (cp.j == cp.n - 1) umma_commit_w(o_done);
+        ++kv_it;
+        ++gp;
+        cp.next(p);
+        if (cs.valid) issue_s();  // S(gp + 1) into the buffer P(gp - 1) just released
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    // ------------------------------------------------------- softmax -----
+    const int half = warp / 4;  // key half / O column half
+    const int wq = warp % 4;    // TMEM lane quarter
+    const int r = wq * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const float sl2 = p.scale_log2;
+    const bool tr = lane == 0 && wq == 0 && half == 0;
+    uint32_t g = 0;
+    int ord = 0;
+    for (long long u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const int h = static_cast<int>(u / p.n_rows);
+      const int ri = static_cast<int>(u % p.n_rows);
+      const int row = p.row_order ? __ldg(p.row_order + ri) : ri;
+      const int beg = __ldg(p.row_ptr + row);
+      const int n = __ldg(p.row_ptr + row + 1) - beg;
+      __nv_bfloat16* orow = p.out + (static_cast<long long>(row) * kBM + r) * p.out_tok_stride +
+                            h * p.out_head_stride + half * (D / 2);
+      if (n == 0) {  // no active block: defined output (zeros); no pipeline traffic
+        uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int v = 0; v < D / 16; ++v) reinterpret_cast<uint4*>(orow)[v] = z;
+        continue;
+      }
+      float m = -INFINITY;  // running max (raw logits), possibly stale
+      float l = 0.f;        // this half's row sum
+      for (int j = 0; j < n; ++j, ++g) {
+        const uint32_t b = g & 1;
+        const uint32_t sb = b * 128;
+        if (tr) RP_TR2(0, g);
+        mbar_wait(&s_full[b], (g >> 1) & 1);
+        if (tr) RP_TR2(1, g);
+        tc_fence_after();
+        uint32_t s0[32], s1[32];
+        tmem_ld32(trow + sb + 64 * half, s0);
+        tmem_ld32(trow + sb + 64 * half + 32, s1);
+        tmem_wait_ld();
+        if (tr) RP_TR2(10, g);
+        auto S = [&](int e) -> float { return __uint_as_float(e < 32 ? s0[e] : s1[e - 32]); };
+        float mq[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float a = S(32 * c);
+#pragma unroll
+          for (int i = 1; i < 31; i += 2) a = fmaxf(a, fmaxf(S(32 * c + i), S(32 * c + i + 1)));
+          mq[c] = fmaxf(a, S(32 * c + 31));
+        }
+        // combine the two halves' maxima of each row (slot g % 2 keeps the
+        // partner's read of this step ahead of our write two steps later)
+        float* slot = red_max + b * 256;
+        slot[half * 128 + r] = fmaxf(mq[0], mq[1]);
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+        const float mx = fmaxf(slot[r], slot[128 + r]);
+        const float m_new = fmaxf(m, mx);
+        bool need = false;
+        float alpha = 1.0f;
+        if (j == 0) {
+          m = m_new;
+        } else if ((m_new - m) * sl2 > 8.0f) {
+          need = true;
+          alpha = ex2((m - m_new) * sl2);
+          m = m_new;
+          l *= alpha;
+        }
+        if (__any_sync(0xFFFFFFFFu, need)) {
+          // O must hold P(g-1).V(g-1) before it is rescaled
+          mbar_wait(pv_done, (g - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) {
+            uint32_t o[32];
+            const uint32_t oc = trow + L::kO + half * (D / 2) + c * 32;
+            tmem_ld32(oc, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(oc, o);
+          }
+        }
+        // p = 2^((s - m) * scale * log2 e): 32 pairs, chunked so a chunk's
+        // exponentials overlap the packing of the previous one.
+        const float2 sc2 = make_float2(sl2, sl2);
+        const float2 ng2 = make_float2(-m * sl2, -m * sl2);
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t pk[32];
+        float2 pv_prev[16];
+#pragma unroll
+        for (int c = 0; c <= 2; ++c) {
+          float2 pv_cur[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (c < 2) {
+              const int e = 32 * c + 2 * i;
+              const float2 xv = ffma2v(make_float2(S(e), S(e + 1)), sc2, ng2);
+              if (kPolyMask & (1u << (i & 7))) {
+                pv_cur[i] = ex2_poly2(xv);
+              } else {
+                pv_cur[i].x = ex2v(xv.x);
+                pv_cur[i].y = ex2v(xv.y);
+              }
+            }
+            if (c > 0) {
+              acc[i & 1] = fadd2v(acc[i & 1], pv_prev[i]);
+              pk[16 * (c - 1) + i] = pack_bf16v(pv_prev[i].x, pv_prev[i].y);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
+        }
+        if (tr) RP_TR2(11, g);
+        const float2 at = fadd2(acc[0], acc[1]);
+        l += at.x + at.y;
+        tmem_st32(trow + sb + 32 * half, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b]);
+        if (tr) RP_TR2(2, g);
+      }
+      // epilogue: wait for the unit's last P.V, combine the halves' sums,
+      // O / l -> bf16 -> global (this half's D/2 columns)
+      red_l[half * 128 + r] = l;
+      mbar_wait(o_done, ord & 1);
+      tc_fence_after();
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+      const float inv = 1.0f / (red_l[r] + red_l[128 + r]);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t o[32];
+        tmem_ld32(trow + L::kO + half * (D / 2) + c * 32, o);
+        tmem_wait_ld();
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 pkt;
+          pkt.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+          pkt.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+          pkt.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+          pkt.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+          dst[v] = pkt;
+        }
+      }
+      tc_fence_before();
+      // red_l is rewritten next unit only after this barrier pair's next
+      // use, which both warps reach after reading it here
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free);
+      ++ord;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace attn2
+}  // namespace rp

@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,6 +19,7 @@
 // instantiation and the launch sites together).
 #include "attn_f32.cu"
 #include "attn_sm100.cu"
+#include "attn_sm100_db.cu"
 #include "csr.cu"
 
 namespace rp {
@@ -64,6 +66,54 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (t->token_stride % 8 || t->head_stride % 8)
         throw std::invalid_argument("sparse attention (bf16): strides must be multiples of 8");
     const CUtensorMap mq = make_map_bf16(q), mk = make_map_bf16(k), mv = make_map_bf16(v);
+    // K6 variant: "db" (default) = one query tile per CTA with the score
+    // tile double-buffered in TMEM (attn_sm100_db.cu); "pair" = two-head
+    // ping-pong (attn_sm100.cu), kept for comparison (DYNRAD_K6=pair).
+    static const bool pair_kernel = [] {
+      const char* e = std::getenv("DYNRAD_K6");
+      return e && std::strcmp(e, "pair") == 0;
+    }();
+    // Both kernels re-balance registers between warpgroups with setmaxnreg;
+    // that only works if the launch allocates the full 168 x 384 pool.
+    auto check_regs = [](const void* fn) {
+      cudaFuncAttributes fa;
+      RP_CUDA(cudaFuncGetAttributes(&fa, fn));
+      if (fa.numRegs * attn::kThreads < 2 * 128 * 208 + 128 * 88)
+        throw CudaError("K6 compiled with too few registers for its setmaxnreg plan");
+    };
+    auto prepare = [&](const void* fn, int smem, bool& done) {
+      if (done) return;
+      check_regs(fn);
+      RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      done = true;
+    };
+    if (!pair_kernel) {
+      attn2::Params p;
+      p.row_ptr = row_ptr;
+      p.col_idx = col_idx;
+      p.row_order = row_order;
+      p.n_rows = static_cast<int>(g.blocks_per_dim);
+      p.heads = q.heads;
+      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
+      p.out = static_cast<__nv_bfloat16*>(o.data);
+      p.out_tok_stride = o.token_stride;
+      p.out_head_stride = o.head_stride;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
+      if (d == 128) {
+        static bool done = false;
+        const int smem = attn2::Layout<128>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<128>), smem, done);
+        attn2::bsfa_fwd_db_kernel<128><<<grid, attn2::kThreads, smem, stream>>>(mq, mk, mv, p);
+      } else {
+        static bool done = false;
+        const int smem = attn2::Layout<64>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<64>), smem, done);
+        attn2::bsfa_fwd_db_kernel<64><<<grid, attn2::kThreads, smem, stream>>>(mq, mk, mv, p);
+      }
+      RP_LAUNCHED();
+      return;
+    }
     attn::Params p;
     p.row_ptr = row_ptr;
     p.col_idx = col_idx;
@@ -77,33 +127,15 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     p.out_head_stride = o.head_stride;
     p.scale_log2 = scale * 1.4426950408889634f;
     const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-    // The kernel re-balances registers between warpgroups with setmaxnreg;
-    // that only works if the launch allocates the full 168 x 384 pool.
-    auto check_regs = [](const void* fn) {
-      cudaFuncAttributes fa;
-      RP_CUDA(cudaFuncGetAttributes(&fa, fn));
-      if (fa.numRegs * attn::kThreads < 2 * 128 * 208 + 128 * 88)
-        throw CudaError("bsfa_fwd_kernel compiled with too few registers for its setmaxnreg plan");
-    };
     if (d == 128) {
-      static bool attr = false;
+      static bool done = false;
       const int smem = attn::Layout<128>::kSmemBytes;
-      if (!attr) {
-        check_regs(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<128>));
-        RP_CUDA(cudaFuncSetAttribute(attn::bsfa_fwd_kernel<128>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-      }
+      prepare(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<128>), smem, done);
       attn::bsfa_fwd_kernel<128><<<grid, attn::kThreads, smem, stream>>>(mq, mk, mv, p);
     } else {
-      static bool attr = false;
+      static bool done = false;
       const int smem = attn::Layout<64>::kSmemBytes;
-      if (!attr) {
-        check_regs(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<64>));
-        RP_CUDA(cudaFuncSetAttribute(attn::bsfa_fwd_kernel<64>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-      }
+      prepare(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<64>), smem, done);
       attn::bsfa_fwd_kernel<64><<<grid, attn::kThreads, smem, stream>>>(mq, mk, mv, p);
     }
     RP_LAUNCHED();
@@ -156,6 +188,44 @@ static void launch_csr(const rp_grid& g, const uint8_t* bits, int32_t* row_ptr, 
   }
 }
 
+// Host-buffer entry point plumbing: two non-blocking copy streams (H2D, D2H)
+// per process, and a stream-ordered pool that keeps its memory between calls
+// (the default release threshold returns every byte at each synchronize, so
+// multi-GB staging buffers would be re-mapped on every call).
+struct HostStreams {
+  cudaStream_t in = nullptr, out = nullptr;
+};
+HostStreams& host_streams() {
+  static HostStreams hs = [] {
+    HostStreams x;
+    RP_CUDA(cudaStreamCreateWithFlags(&x.in, cudaStreamNonBlocking));
+    RP_CUDA(cudaStreamCreateWithFlags(&x.out, cudaStreamNonBlocking));
+    return x;
+  }();
+  return hs;
+}
+void keep_pool_memory() {
+  static bool done = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~uint64_t{0};
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return true;
+  }();
+  (void)done;
+}
+// Head chunks of the host-buffer pipeline (DYNRAD_E2E_CHUNKS, default 4).
+int e2e_chunks() {
+  static const int n = [] {
+    const char* e = std::getenv("DYNRAD_E2E_CHUNKS");
+    const int v = e ? std::atoi(e) : 4;
+    return v > 0 ? v : 4;
+  }();
+  return n;
+}
+
 }  // namespace rp
 
 using namespace rp;
@@ -167,7 +237,10 @@ const char* rp_version(void) { return "dynrad-b200 0.1 (sm_100a)"; }
 int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
 #ifdef RP_TRACE
 int rp_debug_trace(void* host) {
-  return cudaMemcpyFromSymbol(host, attn::g_trace, sizeof(attn::g_trace)) == cudaSuccess ? 0 : 1;
+  const char* e = std::getenv("DYNRAD_K6");
+  if (e && std::strcmp(e, "pair") == 0)
+    return cudaMemcpyFromSymbol(host, attn::g_trace, sizeof(attn::g_trace)) == cudaSuccess ? 0 : 1;
+  return cudaMemcpyFromSymbol(host, attn2::g_trace, sizeof(attn2::g_trace)) == cudaSuccess ? 0 : 1;
 }
 #endif
 
@@ -316,10 +389,12 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_b
       throw std::invalid_argument("masked attention: mask smaller than batch");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t es = dtype == RP_BF16 ? 2 : 4;
-    const size_t in_bytes = static_cast<size_t>(tokens) * heads * head_dim * es;
-    const size_t out_bytes = static_cast<size_t>(g->padded_tokens) * heads * head_dim * es;
+    const size_t row_in = static_cast<size_t>(heads) * head_dim * es;  // bytes per token
+    const size_t in_bytes = static_cast<size_t>(tokens) * row_in;
+    const size_t out_bytes = static_cast<size_t>(g->padded_tokens) * row_in;
     const size_t mask_bytes = static_cast<size_t>(g->blocks_per_dim * g->row_bytes);
     const int64_t nb = g->blocks_per_dim;
+    keep_pool_memory();
     uint8_t *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr, *dm = nullptr;
     int32_t *rp_ = nullptr, *ci = nullptr, *ro = nullptr, *cnt = nullptr;
     int* flag = nullptr;
@@ -335,40 +410,77 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_b
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), b, s));
       fr.ptrs.push_back(*p);
     };
-    alloc(&dq, in_bytes);
-    alloc(&dk, in_bytes);
-    alloc(&dv, in_bytes);
-    alloc(&dout, out_bytes);
     alloc(&dm, mask_bytes);
     alloc(&rp_, sizeof(int32_t) * (nb + 1));
     alloc(&ci, sizeof(int32_t) * nb * nb);
     alloc(&ro, sizeof(int32_t) * nb);
     alloc(&cnt, sizeof(int32_t) * (nb + 1));
     alloc(&flag, sizeof(int));
+    // Row lists first: an empty row is a domain_error in the reference
+    // (attention.cpp:85-86), detected before any feature is moved.
     RP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
-    RP_CUDA(cudaMemcpyAsync(dq, q_host, in_bytes, cudaMemcpyHostToDevice, s));
-    RP_CUDA(cudaMemcpyAsync(dk, k_host, in_bytes, cudaMemcpyHostToDevice, s));
-    RP_CUDA(cudaMemcpyAsync(dv, v_host, in_bytes, cudaMemcpyHostToDevice, s));
     RP_CUDA(cudaMemcpyAsync(dm, mask_bits_host, mask_bytes, cudaMemcpyHostToDevice, s));
     launch_csr(*g, dm, rp_, ci, nb * nb, ro, nullptr, cnt, s);
-    // an empty row is a domain_error in the reference (attention.cpp:85-86)
     std::vector<int32_t> hcnt(static_cast<size_t>(nb) + 1);
     RP_CUDA(cudaMemcpyAsync(hcnt.data(), rp_, sizeof(int32_t) * (nb + 1),
                             cudaMemcpyDeviceToHost, s));
     RP_CUDA(cudaStreamSynchronize(s));
     for (int64_t r = 0; r < nb; ++r)
       if (hcnt[r + 1] == hcnt[r]) throw std::domain_error("masked attention: row has no active key");
-    rp_tensor tq{dq, dtype, tokens, heads, head_dim, static_cast<int64_t>(heads) * head_dim,
-                 head_dim};
-    rp_tensor tk = tq, tv = tq;
-    tk.data = dk;
-    tv.data = dv;
-    rp_tensor to = tq;
-    to.data = dout;
-    to.tokens = g->padded_tokens;
-    launch_attention(*g, tq, tk, tv, to, rp_, ci, ro, 0.f, s, flag);
-    RP_CUDA(cudaMemcpyAsync(o_host, dout, out_bytes, cudaMemcpyDeviceToHost, s));
+    alloc(&dq, in_bytes);
+    alloc(&dk, in_bytes);
+    alloc(&dv, in_bytes);
+    alloc(&dout, out_bytes);
+    // Head-chunk pipeline over three streams: H2D of chunk c+1 and D2H of
+    // chunk c-1 run under the kernel of chunk c (PCIe is full duplex).
+    const int chunks = std::max(1, std::min(heads, e2e_chunks()));
+    const int per = (heads + chunks - 1) / chunks;
+    HostStreams& hs = host_streams();
+    cudaEvent_t start_ev;
+    RP_CUDA(cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming));
+    RP_CUDA(cudaEventRecord(start_ev, s));  // allocations above are ordered on s
+    RP_CUDA(cudaStreamWaitEvent(hs.in, start_ev, 0));
+    std::vector<cudaEvent_t> evs;
+    auto event = [&]() {
+      cudaEvent_t e;
+      RP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      return e;
+    };
+    for (int h0 = 0; h0 < heads; h0 += per) {
+      const int hc = std::min(per, heads - h0);
+      const size_t off = static_cast<size_t>(h0) * head_dim * es;
+      const size_t w = static_cast<size_t>(hc) * head_dim * es;
+      for (auto pr : {std::make_pair(dq, q_host), std::make_pair(dk, k_host),
+                      std::make_pair(dv, v_host)})
+        RP_CUDA(cudaMemcpy2DAsync(pr.first + off, row_in,
+                                  static_cast<const uint8_t*>(pr.second) + off, row_in, w,
+                                  static_cast<size_t>(tokens), cudaMemcpyHostToDevice, hs.in));
+      cudaEvent_t in_done = event();
+      RP_CUDA(cudaEventRecord(in_done, hs.in));
+      RP_CUDA(cudaStreamWaitEvent(s, in_done, 0));
+      const int64_t ts = static_cast<int64_t>(heads) * head_dim;
+      rp_tensor tq{dq + off, dtype, tokens, hc, head_dim, ts, head_dim};
+      rp_tensor tk = tq, tv = tq;
+      tk.data = dk + off;
+      tv.data = dv + off;
+      rp_tensor to = tq;
+      to.data = dout + off;
+      to.tokens = g->padded_tokens;
+      launch_attention(*g, tq, tk, tv, to, rp_, ci, ro, 0.f, s, flag);
+      cudaEvent_t k_done = event();
+      RP_CUDA(cudaEventRecord(k_done, s));
+      RP_CUDA(cudaStreamWaitEvent(hs.out, k_done, 0));
+      RP_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(o_host) + off, row_in, dout + off, row_in,
+                                w, static_cast<size_t>(g->padded_tokens),
+                                cudaMemcpyDeviceToHost, hs.out));
+    }
+    cudaEvent_t out_done = event();
+    RP_CUDA(cudaEventRecord(out_done, hs.out));
+    RP_CUDA(cudaStreamWaitEvent(s, out_done, 0));  // frees below are ordered after the copies
     RP_CUDA(cudaStreamSynchronize(s));
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    cudaEventDestroy(start_ev);
   });
 }
 

@@ -147,47 +147,51 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 4) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------------ TMA producer
+      // (whole warp in uniform control flow, one elected lane issues)
       const uint64_t pol = policy_evict_normal();
       uint32_t kv_it = 0, qcnt = 0;
       int prev_tr = -1;
       for (long long it = it0; it < it1; ++it) {
-        const ScoreItem item = p.items[it];
-        if (item.tr != prev_tr) {
+        const int item_tr = shfl0(p.items[it].tr);
+        const int item_tc = shfl0(p.items[it].tc);
+        if (item_tr != prev_tr) {
           mbar_wait(q_empty, (qcnt & 1) ^ 1);
-          mbar_arrive_expect_tx(q_full, L::kTileBytes);
+          mbar_arrive_expect_tx_w(q_full, L::kTileBytes);
 #pragma unroll
           for (int c = 0; c < NC; ++c)
-            tma_load_3d(sq + c * kChunkBytes, &tq, q_full, (c % p.cph) * 64, c / p.cph,
-                        item.tr * 128, pol);
+            tma_load_3d_w(sq + c * kChunkBytes, &tq, q_full, (c % p.cph) * 64, c / p.cph,
+                        item_tr * 128, pol);
           ++qcnt;
-          prev_tr = item.tr;
+          prev_tr = item_tr;
         }
         const uint32_t st = kv_it % L::kStages;
         mbar_wait(&kv_empty[st], ((kv_it / L::kStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], L::kTileBytes);
+        mbar_arrive_expect_tx_w(&kv_full[st], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-          tma_load_3d(sk + st * L::kTileBytes + c * kChunkBytes, &tk, &kv_full[st],
-                      (c % p.cph) * 64, c / p.cph, item.tc * 128, pol);
+          tma_load_3d_w(sk + st * L::kTileBytes + c * kChunkBytes, &tk, &kv_full[st],
+                      (c % p.cph) * 64, c / p.cph, item_tc * 128, pol);
         ++kv_it;
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------------- MMA issuer
+      // (whole warp: descriptors stay in uniform registers, see common.cuh)
       const uint32_t idesc = idesc_bf16(128, 128, false, false);
       const uint32_t qa = smem_u32(sq), kb0 = smem_u32(sk);
       uint32_t kv_it = 0, qcnt = 0, n = 0;
       int prev_tr = -1;
       for (long long it = it0; it < it1; ++it, ++n) {
-        const ScoreItem item = p.items[it];
-        if (item.tr != prev_tr) {
-          if (prev_tr >= 0) umma_commit(q_empty);  // old Q' no longer read
+        const int item_tr = shfl0(p.items[it].tr);
+        const int item_tc = shfl0(p.items[it].tc);
+        if (item_tr != prev_tr) {
+          if (prev_tr >= 0) umma_commit_w(q_empty);  // old Q' no longer read
           mbar_wait(q_full, qcnt & 1);
           ++qcnt;
-          prev_tr = item.tr;
+          prev_tr = item_tr;
         }
         const uint32_t st = kv_it % L::kStages;
         const uint32_t buf = n & 1;
@@ -198,11 +202,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < NC * 4; ++kk) {
           const uint32_t off = (kk / 4) * kChunkBytes + (kk % 4) * 32;
-          umma_ss(tmem + buf * 128, smem_desc_sw128(qa + off, 0, 1024),
+          umma_ss_w(tmem + buf * 128, smem_desc_sw128(qa + off, 0, 1024),
                   smem_desc_sw128(kb + off, 0, 1024), idesc, kk > 0);
         }
-        umma_commit(&kv_empty[st]);
-        umma_commit(&s_full[buf]);
+        umma_commit_w(&kv_empty[st]);
+        umma_commit_w(&s_full[buf]);
         ++kv_it;
       }
     }

@@ -97,3 +97,26 @@ def test_static_select_stream_matches_reference(ref):
     assert len(uv) == 13  # |P| = 52
     assert len({tuple(x) for x in uv}) == 13
     assert all(abs(u - v) <= 4 for u, v in uv)
+
+
+def test_reference_library_and_oracle_disagree_on_disable_split(ref):
+    """With BuildOptions::disable_split, the reference's build_mask gives
+    split-pruned frame pairs an empty candidate set (candidate_set keeps
+    retained=false, radial.cpp:111-121) while its own brute-force
+    oracle::build scores their full band (tests/oracle.cpp:190-197).  Parity
+    for disable_split is therefore pinned to the library (the GPU follows it,
+    tests/test_mask_gpu.py golden '-nosplit' cases), not to oracle::build.
+    (Static mode with disable_split divides by zero in the reference, SIGFPE;
+    the GPU path raises InvalidArgument instead.)"""
+    differ = 0
+    for seed in range(5):
+        cfg = pyoracle.Cfg(1, 1.0, 0.1, 1e-6, 0.3, 0.3, -0.5, -0.5, 1)
+        q, k, _ = ref.random_batch(6 * 8, 2, 8, seed, with_values=False)
+        lib = ref.build_mask(6, 8, 4, cfg, 7, disable_split=True, q=q, k=k)
+        orc = pyoracle.pack_dense(ref.oracle_build(6, 8, 4, cfg, 7, disable_split=True, q=q, k=k))
+        same_split = np.array_equal(
+            ref.build_mask(6, 8, 4, cfg, 7, q=q, k=k),
+            pyoracle.pack_dense(ref.oracle_build(6, 8, 4, cfg, 7, q=q, k=k)))
+        assert same_split
+        differ += not np.array_equal(np.asarray(lib), np.asarray(orc))
+    assert differ == 5
