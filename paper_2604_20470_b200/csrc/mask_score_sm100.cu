@@ -63,7 +63,7 @@ struct SParams {
   unsigned long long* queue_len;
   long long queue_cap;
   const float* qnorm;
-  const float* knorm;
+  const float* kmax;  // per 128-token tile: max |k'_v|
   float kappa;
   float delta_floor;
   Feat feat;  // exact re-score in place when the recheck queue is full
@@ -78,7 +78,7 @@ struct SLayout {
   static constexpr int kStages = 2;
   static constexpr int kSmemData = (1 + kStages) * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 6;
-  // bars | tmem slot (16 B) | knorm[128] | wcnt[4][128] | red[4][3] doubles
+  // bars | tmem slot (16 B) | (unused 512 B) | wcnt[4][128] | red[4][3] doubles
   static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 4 * 128 * 4 + 4 * 3 * 8;
   static constexpr int kSmemBytes = kSmemData + kExtra + 1024;
 };
@@ -100,6 +100,19 @@ RP_DEV Welford chan(Welford a, Welford b) {
   return r;
 }
 
+// Undecided pair: append to the recheck queue, or -- if the queue is full --
+// decide it right here with the exact fp64 score.  Out of line so the
+// epilogue's unrolled loops stay compact.  Returns true iff kept now.
+__device__ __noinline__ bool queue_or_decide(const SParams& p, int job, const DJob& jb, int u,
+                                             int v, long long gr, long long kj, double2 st) {
+  const unsigned long long slot = atomicAdd(p.queue_len, 1ull);
+  if (slot < static_cast<unsigned long long>(p.queue_cap)) {
+    p.queue[slot] = make_int4(job, u, v, 0);
+    return false;
+  }
+  return zscore(exact_score(p.feat, gr, kj + v), st) >= jb.param;
+}
+
 template <int NC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     score_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -118,8 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_full = q_full + 2;   // [2]
   uint64_t* s_empty = q_full + 4;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
-  float* knorm_s = reinterpret_cast<float*>(tmem_slot + 4);     // [128]
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(knorm_s + 128);  // [4][128]
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(tmem_slot + 4 + 128);  // [4][128]
   double* red = reinterpret_cast<double*>(wcnt + 4 * 128);      // [4][3]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -212,6 +224,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ----------------------------------------------------------- epilogue
+    // Branch-free over the 128 columns of the thread's row: the unrolled
+    // loops carry no calls or rare-path code, so the kernel stays small
+    // enough for the instruction cache (an earlier version that inlined the
+    // exact re-score into every unrolled column ran at IPC 0.26, stalled on
+    // instruction fetch).
     const int r = warp * 32 + lane;  // row within the tile
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     uint32_t n = 0;
@@ -219,7 +236,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const ScoreItem item = p.items[it];
       const DJob jb = p.jobs[item.job];
       const uint32_t buf = n & 1;
-      if (MODE == 1) knorm_s[r] = __ldg(p.knorm + static_cast<long long>(item.tc) * 128 + r);
       mbar_wait(&s_full[buf], (n >> 1) & 1);
       tc_fence_after();
       uint32_t sv[4][32];
@@ -241,102 +257,126 @@ __global__ void __launch_bounds__(kThreads, 1)
         c_lo = static_cast<int>(max(kj + vlo - g0, 0ll));
         c_hi = static_cast<int>(min(kj + vhi - g0, 127ll));
       }
+      uint32_t inm[4];
+#pragma unroll
+      for (int w4 = 0; w4 < 4; ++w4) {
+        const int lo = max(c_lo - 32 * w4, 0), hi = min(c_hi - 32 * w4, 31);
+        inm[w4] = lo > hi ? 0u : ((hi == 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+      }
+      const int cnt = c_hi >= c_lo ? c_hi - c_lo + 1 : 0;
       if (MODE == 0) {
-        // two-pass (n, mean, M2) over this row's valid scores
-        float sum = 0.f;
+        // per-row sum and sum of squares of the valid scores (fp32, four
+        // independent chains), then (n, sum, sumsq) reduced in fp64
+        float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < 128; ++c) {
-          const float s = __uint_as_float(sv[c / 32][c % 32]) * p.score_scale;
-          if (c >= c_lo && c <= c_hi) sum += s;
+          const float x = (inm[c / 32] >> (c % 32)) & 1u
+                              ? __uint_as_float(sv[c / 32][c % 32]) * p.score_scale : 0.f;
+          a1[c & 3] += x;
+          a2[c & 3] = fmaf(x, x, a2[c & 3]);
         }
-        const int cnt = c_hi >= c_lo ? c_hi - c_lo + 1 : 0;
-        const float mean = cnt ? sum / static_cast<float>(cnt) : 0.f;
-        float m2 = 0.f;
+        double t1 = static_cast<double>((a1[0] + a1[1]) + (a1[2] + a1[3]));
+        double t2 = static_cast<double>((a2[0] + a2[1]) + (a2[2] + a2[3]));
+        double tn = static_cast<double>(cnt);
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const float d = __uint_as_float(sv[c / 32][c % 32]) * p.score_scale - mean;
-          if (c >= c_lo && c <= c_hi) m2 = fmaf(d, d, m2);
-        }
-        Welford w{static_cast<double>(cnt), static_cast<double>(mean), static_cast<double>(m2)};
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          Welford x{__shfl_xor_sync(0xFFFFFFFFu, w.n, o), __shfl_xor_sync(0xFFFFFFFFu, w.mean, o),
-                    __shfl_xor_sync(0xFFFFFFFFu, w.m2, o)};
-          w = (lane & o) ? chan(x, w) : chan(w, x);  // fixed order -> deterministic
+        for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly -> deterministic lane 0
+          t1 += __shfl_xor_sync(0xFFFFFFFFu, t1, o);
+          t2 += __shfl_xor_sync(0xFFFFFFFFu, t2, o);
+          tn += __shfl_xor_sync(0xFFFFFFFFu, tn, o);
         }
         if (lane == 0) {
-          red[warp * 3 + 0] = w.n;
-          red[warp * 3 + 1] = w.mean;
-          red[warp * 3 + 2] = w.m2;
+          red[warp * 3 + 0] = tn;
+          red[warp * 3 + 1] = t1;
+          red[warp * 3 + 2] = t2;
         }
         epi_bar();
         if (r == 0) {
-          Welford a{red[0], red[1], red[2]};
-          for (int x = 1; x < 4; ++x) a = chan(a, Welford{red[3 * x], red[3 * x + 1], red[3 * x + 2]});
-          p.item_stats[3 * it + 0] = a.n;
-          p.item_stats[3 * it + 1] = a.mean;
-          p.item_stats[3 * it + 2] = a.m2;
+          double N = 0.0, S1 = 0.0, S2 = 0.0;
+          for (int x = 0; x < 4; ++x) {
+            N += red[3 * x];
+            S1 += red[3 * x + 1];
+            S2 += red[3 * x + 2];
+          }
+          const double mean = N > 0.0 ? S1 / N : 0.0;
+          p.item_stats[3 * it + 0] = N;
+          p.item_stats[3 * it + 1] = mean;
+          p.item_stats[3 * it + 2] = N > 0.0 ? fmax(S2 - S1 * mean, 0.0) : 0.0;
         }
         epi_bar();
       } else {
+        // Decision thresholds of this row in raw accumulator units.  The
+        // fast score differs from the reference's by at most
+        // kappa |q'_u| |k'_v| (fp32 accumulation) plus the mu/sigma and
+        // float-rounding floor delta (1 + |z|); only |z - tau| < 1 can be
+        // undecided, so B = qn * kmax(tile) + delta (2 + |tau|) bounds it.
         const double2 st = p.job_stats[item.job];
-        const double invd = 1.0 / (st.y + 1e-8);
-        const float muf = static_cast<float>(st.x);
-        const float inv = static_cast<float>(invd);
-        const float tau = static_cast<float>(jb.param);
-        const float qn = __ldg(p.qnorm + gr) * p.kappa * p.score_scale * inv;
-        epi_bar();  // knorm_s ready
-        uint32_t keep[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          if (c < c_lo || c > c_hi) continue;
-          const float s = __uint_as_float(sv[c / 32][c % 32]) * p.score_scale;
-          const float z = (s - muf) * inv;
-          // error bound in z units: accumulation bound + mu/sigma/rounding floor
-          const float bound = fmaf(qn, knorm_s[c], p.delta_floor * (1.f + fabsf(z)));
-          const float dz = z - tau;
-          if (dz >= bound) {
-            keep[c / 32] |= 1u << (c % 32);
-          } else if (dz > -bound) {
-            const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 + c - kj);
-            const unsigned long long slot = atomicAdd(p.queue_len, 1ull);
-            if (slot < static_cast<unsigned long long>(p.queue_cap)) {
-              p.queue[slot] = make_int4(item.job, static_cast<int>(u), v, 0);
-            } else if (zscore(exact_score(p.feat, gr, kj + v), st) >= jb.param) {
-              keep[c / 32] |= 1u << (c % 32);  // queue full: decide exactly here
-            }
-          }
-        }
-        // per-column counts within each warp (32 rows), then per block row
+        const double sd = st.y + 1e-8;
+        const double tau = jb.param;
+        const double B = static_cast<double>(__ldg(p.qnorm + gr)) * p.kappa * p.score_scale / sd *
+                             __ldg(p.kmax + item.tc) +
+                         p.delta_floor * (2.0 + fabs(tau));
+        const float hi_raw = __double2float_ru(((tau + B) * sd + st.x) / p.score_scale);
+        const float lo_raw = __double2float_rd(((tau - B) * sd + st.x) / p.score_scale);
+        uint32_t kb[4], ub[4];
 #pragma unroll
         for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t k1 = 0u, u1 = 0u;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const uint32_t b = __ballot_sync(0xFFFFFFFFu, (keep[w4] >> c) & 1u);
-            if (lane == c) wcnt[warp * 128 + w4 * 32 + c] = __popc(b);
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(sv[w4][i]);
+            k1 |= (x >= hi_raw ? 1u : 0u) << i;
+            u1 |= (x > lo_raw ? 1u : 0u) << i;
           }
+          kb[w4] = k1 & inm[w4];
+          ub[w4] = u1 & inm[w4] & ~k1;
+        }
+        // rare path: queue the undecided pairs for the exact fp64 re-score
+#pragma unroll 1
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t m = ub[w4];
+          while (m) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1;
+            const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 + 32 * w4 + i - kj);
+            if (queue_or_decide(p, item.job, jb, static_cast<int>(u), v, gr, kj, st))
+              kb[w4] |= 1u << i;
+          }
+        }
+        // per-column counts within the warp: transpose each 32 x 32 bit block
+        // (lane = row -> lane = column) and count
+        unsigned long long kept_total = 0;
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          uint32_t x = kb[w4];
+          kept_total += __popc(x);
+#pragma unroll
+          for (int j = 16; j > 0; j >>= 1) {
+            const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu
+                             : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u : 0x55555555u;
+            const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+            x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+          }
+          wcnt[warp * 128 + w4 * 32 + lane] = __popc(x);
         }
         epi_bar();
         // thread r owns column r: sum the warps of each block row
         const int bs = p.bs;
         const int rows_per_blk = bs < 128 ? bs : 128;  // bs in {32, 64, 128}
         const int wpb = rows_per_blk / 32;             // warps per block row
-        unsigned long long kept_total = 0;
         const long long gc = static_cast<long long>(item.tc) * 128 + r;
         for (int br = 0; br < 128 / rows_per_blk; ++br) {
-          uint32_t cnt = 0;
-          for (int x = 0; x < wpb; ++x) cnt += wcnt[(br * wpb + x) * 128 + r];
-          kept_total += cnt;
+          uint32_t c2 = 0;
+          for (int x = 0; x < wpb; ++x) c2 += wcnt[(br * wpb + x) * 128 + r];
           const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
           const long long Cb = gc / bs;
           const long long rr = R - jb.r0, cc = Cb - jb.c0;
-          if (rr >= 0 && rr < jb.tr && cc >= 0 && cc < jb.tc && cnt)
-            p.counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs] = cnt;
+          if (rr >= 0 && rr < jb.tr && cc >= 0 && cc < jb.tc && c2)
+            p.counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs] = c2;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) kept_total += __shfl_xor_sync(0xFFFFFFFFu, kept_total, o);
         if (lane == 0 && kept_total) atomicAdd(&p.job_kept[item.job], kept_total);
-        epi_bar();  // wcnt / knorm_s reuse
+        epi_bar();  // wcnt reuse
       }
     }
   }
@@ -378,6 +418,22 @@ __global__ void job_stats_kernel(const double* __restrict__ item_stats,
     a = chan(a, Welford{item_stats[3 * it], item_stats[3 * it + 1], item_stats[3 * it + 2]});
   const double sd = a.n > 0 ? sqrt(a.m2 / a.n) : 0.0;
   job_stats[j] = make_double2(a.mean, sd);
+}
+
+// Max of the per-token norms over each 128-token tile (one warp per tile).
+__global__ void tile_max_kernel(const float* __restrict__ norms, long long tokens,
+                                long long tiles, float* __restrict__ out) {
+  const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (t >= tiles) return;
+  float m = 0.f;
+  for (int x = lane; x < 128; x += 32) {
+    const long long i = t * 128 + x;
+    if (i < tokens) m = fmaxf(m, norms[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if (lane == 0) out[t] = m;
 }
 
 // Exact re-score of every queued pair (reference operation order).
@@ -495,6 +551,7 @@ class FastEngine {
   long long queue_cap = 0;
   float* d_qn = nullptr;
   float* d_kn = nullptr;
+  float* d_kmax = nullptr;
 
   ~FastEngine() {
     for (void* p : {static_cast<void*>(d_jobs), static_cast<void*>(d_items),
@@ -502,7 +559,7 @@ class FastEngine {
                     static_cast<void*>(d_counts), static_cast<void*>(d_item_stats),
                     static_cast<void*>(d_job_stats), static_cast<void*>(d_kept),
                     static_cast<void*>(d_queue), static_cast<void*>(d_qn),
-                    static_cast<void*>(d_kn)})
+                    static_cast<void*>(d_kn), static_cast<void*>(d_kmax)})
       if (p) cudaFree(p);
   }
 };
@@ -577,6 +634,7 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
   dalloc(&e->d_queue, static_cast<size_t>(e->queue_cap));
   dalloc(&e->d_qn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kn, static_cast<size_t>(g.padded_tokens));
+  dalloc(&e->d_kmax, static_cast<size_t>((g.padded_tokens + 127) / 128));
   RP_CUDA(cudaMemcpy(e->d_jobs, e->jobs.data(), sizeof(DJob) * nj, cudaMemcpyHostToDevice));
   RP_CUDA(cudaMemcpy(e->d_items, e->items.data(), sizeof(ScoreItem) * e->items.size(),
                      cudaMemcpyHostToDevice));
@@ -635,6 +693,10 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   norm_kernel<<<ngrid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k->data), g.total_tokens,
                                     k->token_stride, k->head_stride, e->heads, e->dim, e->d_kn);
   RP_LAUNCHED();
+  const long long ktiles = (g.padded_tokens + 127) / 128;
+  tile_max_kernel<<<static_cast<unsigned>((ktiles + 7) / 8), 256, 0, s>>>(e->d_kn, g.total_tokens,
+                                                                         ktiles, e->d_kmax);
+  RP_LAUNCHED();
 
   SParams p{};
   p.jobs = e->d_jobs;
@@ -652,7 +714,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.queue_len = e->d_kept + nj;
   p.queue_cap = e->queue_cap;
   p.qnorm = e->d_qn;
-  p.knorm = e->d_kn;
+  p.kmax = e->d_kmax;
   // fp32 accumulation of K = H_f * d exact bf16 products, each rounding
   // (or truncating) step off by <= 2^-23 relative: |err| <= 2 K 2^-23
   // sum|q k| <= 2 K 2^-23 |q| |k|.
