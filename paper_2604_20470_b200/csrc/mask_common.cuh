@@ -68,15 +68,33 @@ RP_DEV float feat_at(const void* p, int dtype, int64_t idx) {
 }
 
 // selection.cpp:104-121: per-head dot in double (ascending d), acc +=
-// dot * inv_sqrt_d (no contraction), float(acc / heads).
+// dot * inv_sqrt_d (no contraction), float(acc / heads).  bf16 rows that are
+// 16-byte aligned are read 8 values per load; the accumulation order is the
+// reference's either way.
 RP_DEV float exact_score(const Feat& f, int64_t qrow, int64_t krow) {
   double acc = 0.0;
   for (int h = 0; h < f.heads; ++h) {
     const int64_t qb = qrow * f.q_ts + h * f.q_hs, kb = krow * f.k_ts + h * f.k_hs;
     double dot = 0.0;
-    for (int e = 0; e < f.d; ++e)
-      dot = __fma_rn(static_cast<double>(feat_at(f.q, f.dtype, qb + e)),
-                     static_cast<double>(feat_at(f.k, f.dtype, kb + e)), dot);
+    if (f.dtype == RP_BF16 && ((qb | kb | f.d) & 7) == 0) {
+      const uint4* qv = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(f.q) + qb);
+      const uint4* kv = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(f.k) + kb);
+      for (int e = 0; e < f.d / 8; ++e) {
+        const uint4 a = __ldg(qv + e), b = __ldg(kv + e);
+        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          dot = __fma_rn(static_cast<double>(__uint_as_float(aw[t] << 16)),
+                         static_cast<double>(__uint_as_float(bw[t] << 16)), dot);
+          dot = __fma_rn(static_cast<double>(__uint_as_float(aw[t] & 0xFFFF0000u)),
+                         static_cast<double>(__uint_as_float(bw[t] & 0xFFFF0000u)), dot);
+        }
+      }
+    } else {
+      for (int e = 0; e < f.d; ++e)
+        dot = __fma_rn(static_cast<double>(feat_at(f.q, f.dtype, qb + e)),
+                       static_cast<double>(feat_at(f.k, f.dtype, kb + e)), dot);
+    }
     acc = __dadd_rn(acc, __dmul_rn(dot, f.inv_sqrt_d));
   }
   return __double2float_rn(__ddiv_rn(acc, static_cast<double>(f.heads)));

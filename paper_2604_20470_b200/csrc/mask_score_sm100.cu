@@ -57,6 +57,7 @@ struct SParams {
   float score_scale;     // inv_sqrt_d / H_f
   double* item_stats;    // pass 1: [n_items][3] (n, mean, M2)
   const double2* job_stats;  // pass 2: mean, stddev per job
+  const float2* job_thr;     // pass 2: (raw-unit threshold, raw-unit delta margin) per job
   uint32_t* counts;
   unsigned long long* job_kept;
   int4* queue;
@@ -232,11 +233,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = warp * 32 + lane;  // row within the tile
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     uint32_t n = 0;
+    // Item metadata is prefetched one item ahead (item -> job is a dependent
+    // global load pair that would otherwise sit on every item's critical path).
+    ScoreItem item_nx{};
+    DJob jb_nx{};
+    if (it0 < it1) {
+      item_nx = p.items[it0];
+      jb_nx = p.jobs[item_nx.job];
+    }
     for (long long it = it0; it < it1; ++it, ++n) {
-      const ScoreItem item = p.items[it];
-      const DJob jb = p.jobs[item.job];
+      const ScoreItem item = item_nx;
+      const DJob jb = jb_nx;
+      if (it + 1 < it1) item_nx = p.items[it + 1];
+      const long long gr = static_cast<long long>(item.tr) * 128 + r;
+      float2 thr = make_float2(0.f, 0.f);
+      float qk = 0.f;
+      if (MODE == 1) {
+        thr = p.job_thr[item.job];
+        qk = __ldg(p.qnorm + gr) * p.kappa * __ldg(p.kmax + item.tc);
+      }
       const uint32_t buf = n & 1;
       mbar_wait(&s_full[buf], (n >> 1) & 1);
+      if (it + 1 < it1) jb_nx = p.jobs[item_nx.job];
       tc_fence_after();
       uint32_t sv[4][32];
 #pragma unroll
@@ -246,7 +264,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[buf]);
       // valid columns of this row: contiguous [c_lo, c_hi] (band + frames)
-      const long long gr = static_cast<long long>(item.tr) * 128 + r;
       const long long qi = static_cast<long long>(jb.i) * p.nt;
       const long long kj = static_cast<long long>(jb.j) * p.nt;
       const long long u = gr - qi;
@@ -308,15 +325,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // fast score differs from the reference's by at most
         // kappa |q'_u| |k'_v| (fp32 accumulation) plus the mu/sigma and
         // float-rounding floor delta (1 + |z|); only |z - tau| < 1 can be
-        // undecided, so B = qn * kmax(tile) + delta (2 + |tau|) bounds it.
-        const double2 st = p.job_stats[item.job];
-        const double sd = st.y + 1e-8;
-        const double tau = jb.param;
-        const double B = static_cast<double>(__ldg(p.qnorm + gr)) * p.kappa * p.score_scale / sd *
-                             __ldg(p.kmax + item.tc) +
-                         p.delta_floor * (2.0 + fabs(tau));
-        const float hi_raw = __double2float_ru(((tau + B) * sd + st.x) / p.score_scale);
-        const float lo_raw = __double2float_rd(((tau - B) * sd + st.x) / p.score_scale);
+        // undecided, so in z units B = qn kmax(tile) kappa scale / sd +
+        // delta (2 + |tau|).  In raw units z >= tau + B <=> raw >= base + m
+        // with base = (tau sd + mu) / scale and m = qn kmax kappa + c_job
+        // (job_stats_kernel); the fp32 evaluation is inflated by 2^-20
+        // relative so rounding can only widen the undecided band.
+        const float m = fmaf(qk, 1.f + 0x1p-20f, thr.y) + 0x1p-20f * fabsf(thr.x);
+        const float hi_raw = thr.x + m;
+        const float lo_raw = thr.x - m;
+        const double2 st = p.job_stats[item.job];  // for the rare exact decisions
         uint32_t kb[4], ub[4];
 #pragma unroll
         for (int w4 = 0; w4 < 4; ++w4) {
@@ -410,7 +427,9 @@ __global__ void norm_kernel(const __nv_bfloat16* __restrict__ x, long long token
 // Deterministic per-frame-pair merge of item statistics (fixed item order).
 __global__ void job_stats_kernel(const double* __restrict__ item_stats,
                                  const long long* __restrict__ job_item_off, int n_jobs,
-                                 double2* __restrict__ job_stats) {
+                                 const DJob* __restrict__ jobs, double score_scale,
+                                 double delta_floor, double2* __restrict__ job_stats,
+                                 float2* __restrict__ job_thr) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_jobs) return;
   Welford a{0.0, 0.0, 0.0};
@@ -418,6 +437,10 @@ __global__ void job_stats_kernel(const double* __restrict__ item_stats,
     a = chan(a, Welford{item_stats[3 * it], item_stats[3 * it + 1], item_stats[3 * it + 2]});
   const double sd = a.n > 0 ? sqrt(a.m2 / a.n) : 0.0;
   job_stats[j] = make_double2(a.mean, sd);
+  // pass-2 thresholds in raw accumulator units (see score_kernel)
+  const double tau = jobs[j].param, sde = sd + 1e-8;
+  job_thr[j] = make_float2(__double2float_rn((tau * sde + a.mean) / score_scale),
+                           __double2float_ru(delta_floor * (2.0 + fabs(tau)) * sde / score_scale));
 }
 
 // Max of the per-token norms over each 128-token tile (one warp per tile).
@@ -546,6 +569,7 @@ class FastEngine {
   uint32_t* d_counts = nullptr;
   double* d_item_stats = nullptr;
   double2* d_job_stats = nullptr;
+  float2* d_job_thr = nullptr;
   unsigned long long* d_kept = nullptr;  // [jobs + 1]: per job, then queue length
   int4* d_queue = nullptr;
   long long queue_cap = 0;
@@ -558,6 +582,7 @@ class FastEngine {
                     static_cast<void*>(d_job_item_off), static_cast<void*>(d_tiles),
                     static_cast<void*>(d_counts), static_cast<void*>(d_item_stats),
                     static_cast<void*>(d_job_stats), static_cast<void*>(d_kept),
+                    static_cast<void*>(d_job_thr),
                     static_cast<void*>(d_queue), static_cast<void*>(d_qn),
                     static_cast<void*>(d_kn), static_cast<void*>(d_kmax)})
       if (p) cudaFree(p);
@@ -625,6 +650,7 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
   dalloc(&e->d_counts, static_cast<size_t>(off));
   dalloc(&e->d_item_stats, 3 * e->items.size());
   dalloc(&e->d_job_stats, nj);
+  dalloc(&e->d_job_thr, nj);
   dalloc(&e->d_kept, nj + 1);
   // recheck queue: 1% of the scored pairs (expected ~0.1%); pairs beyond
   // the capacity are re-scored in place by the select pass.
@@ -708,6 +734,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.score_scale = static_cast<float>((1.0 / std::sqrt(static_cast<double>(e->dim))) / e->heads);
   p.item_stats = e->d_item_stats;
   p.job_stats = e->d_job_stats;
+  p.job_thr = e->d_job_thr;
   p.counts = e->d_counts;
   p.job_kept = e->d_kept;
   p.queue = e->d_queue;
@@ -734,7 +761,8 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
     }
     if (mode == 0) {
       job_stats_kernel<<<(nj + 127) / 128, 128, 0, s>>>(e->d_item_stats, e->d_job_item_off, nj,
-                                                       e->d_job_stats);
+                                                       e->d_jobs, p.score_scale, delta_floor,
+                                                       e->d_job_stats, e->d_job_thr);
       RP_LAUNCHED();
     }
   }

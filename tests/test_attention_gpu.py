@@ -141,3 +141,66 @@ def test_fp32_empty_row_is_domain_error(cuda):
     q = np.ones((128, 1, 8), np.float32)
     with pytest.raises(rp.DomainError):
         rp.masked_attention_exact(g, m, q, q, q)
+
+
+def test_wan_shape_bf16_vs_oracle_sampled_rows(cuda, port):
+    """Production shape (Wan2.1 21x3600, B=128, config-3 static mask, 0.8061
+    sparsity): the tcgen05 kernel against the C restatement of
+    attention.cpp:50-106 on sampled query rows spread over the sequence
+    (the full CPU evaluation would take ~23 min per head)."""
+    g = rp.make_grid(21, 3600, 128)
+    cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(1.0, 0.1), 1.0, 0.2, 0.3, 0.3)
+    mask = rp.Plan(g, cfg, 7).build_mask_device()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mask)
+    assert int(col_idx.numel()) == 67743
+    H, d, S = 2, 128, g.total_tokens
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn((S, H, d), device="cuda", generator=gen).to(torch.bfloat16)
+               for _ in range(3))
+    out = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order).float().cpu().numpy()
+    qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))
+    bits = mask.cpu().numpy()
+    worst = 0.0
+    for r0 in (0, 3590, 20000, 41000, 61234, 75600 - 8, 75640):  # incl. the padded tail
+        r1 = min(r0 + 8, g.padded_tokens)
+        ref = port.masked_attention_exact(21, 3600, 128, bits, qn, kn, vn, r0, r1, threads=8)
+        worst = max(worst, rel_rows(out[r0:r1], ref))
+    assert worst < 2e-2, worst
+
+
+def test_empty_row_gives_zeros_on_device(cuda):
+    """The device entry point cannot raise mid-stream: a block row with no
+    active block is written as zeros (the host/facade entry points raise the
+    reference's domain_error instead, test_fp32_empty_row_is_domain_error)."""
+    g = rp.make_grid(2, 256, 128)
+    dense = np.eye(4, dtype=np.uint8)
+    dense[2, 2] = 0
+    bits = pyoracle.pack_dense(dense)
+    row_ptr, col_idx, order = rp.mask_to_csr(g, torch.from_numpy(bits).cuda())
+    torch.manual_seed(3)
+    q, k, v = (torch.randn(512, 2, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
+    out = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order).float()
+    assert torch.count_nonzero(out[256:384]) == 0
+    ref = _torch_ref(q, k, v, np.eye(4, dtype=np.uint8), 128, 512)
+    keep = torch.ones(512, dtype=torch.bool, device="cuda")
+    keep[256:384] = False
+    assert rel_rows(out[keep].cpu().numpy(), ref[keep].cpu().numpy()) < 2e-2
+
+
+def test_host_pipeline_matches_device_path(cuda):
+    """rp_masked_attention_exact_host (head-chunked H2D / kernel / D2H over
+    three streams, strided head views) equals the device entry point."""
+    g = rp.make_grid(3, 700, 128)
+    S, H, d = g.total_tokens, 6, 128
+    dense = _random_mask(g.blocks_per_dim, 0.5, 11)
+    bits = pyoracle.pack_dense(dense)
+    rng = np.random.default_rng(2)
+    x = [torch.from_numpy(rng.standard_normal((S, H, d), dtype=np.float32)).to(torch.bfloat16)
+         for _ in range(3)]
+    mask = rp.BlockMask(g.blocks_per_dim, bits)
+    host = rp.masked_attention_exact(
+        g, mask, *(t.view(torch.int16).numpy().view(np.uint16) for t in x))
+    host = torch.from_numpy(host.view(np.int16)).view(torch.bfloat16)
+    row_ptr, col_idx, order = rp.mask_to_csr(g, torch.from_numpy(bits).cuda())
+    dev = rp.sparse_attention(g, *(t.cuda() for t in x), row_ptr, col_idx, order).cpu()
+    assert torch.equal(host, dev)

@@ -1,0 +1,74 @@
+"""BASELINE.json configs[4]: lambda / sparsity sweep at the Wan2.1-14B shape
+(21x45x80 = 75,600 tokens, 40 heads, d=128, bf16, B=128) on one B200: stage-(d)
+ms per layer, TFLOP/s on active blocks and fraction of the measured bf16 peak,
+next to dense bf16 attention (our kernel on a full mask, and torch SDPA).
+Static-ratio masks (SURVEY 6.3 points; 90-95 % is unreachable under the
+reference semantics).  Writes one JSON document to stdout."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2604_20470_b200 import radialplan as rp
+
+POINTS = [  # gamma, lambda, theta_m, theta_c, rho1, rho2   (reference sparsity)
+    (2.0, 0.3, 0.75, 0.2, 0.25, 0.55),   # Table-3 Low, 0.532
+    (2.0, 0.1, 0.75, 0.2, 0.3, 0.3),     # 0.638
+    (1.0, 0.3, 0.75, 0.2, 0.3, 0.3),     # 0.682
+    (1.0, 0.15, 0.75, 0.2, 0.3, 0.3),    # 0.705
+    (1.0, 0.1, 0.75, 0.2, 0.3, 0.3),     # 0.738
+    (1.0, 0.1, 1.0, 0.2, 0.3, 0.3),      # config 3, 0.8061
+    (0.5, 0.05, 0.75, 0.2, 0.3, 0.3),    # 0.829
+    (1.0, 0.001, 1.0, 1.0, 1e-9, 1e-9),  # maximum, 0.8646
+]
+
+
+def timed(fn, reps=5):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json")))["bf16_tflops"]
+    g = rp.make_grid(21, 3600, 128)
+    H, d, S = 40, 128, g.total_tokens
+    gen = torch.Generator(device="cuda").manual_seed(42)
+    q, k, v = (torch.randn((S, H, d), device="cuda", generator=gen).to(torch.bfloat16)
+               for _ in range(3))
+    out = torch.empty((g.padded_tokens, H, d), device="cuda", dtype=torch.bfloat16)
+    nb = g.blocks_per_dim
+    full = torch.from_numpy(np.packbits(np.ones((nb, nb), np.uint8), axis=1,
+                                        bitorder="little")).cuda()
+    rpf, cif, orf = rp.mask_to_csr(g, full)
+    dense_ms = timed(lambda: rp.sparse_attention(g, q, k, v, rpf, cif, orf, out=out), 2)
+    qs, ks, vs = (t.permute(1, 0, 2).unsqueeze(0) for t in (q, k, v))
+    sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs), 2)
+    rows = []
+    for (gm, lm, tm, tc, a, b) in POINTS:
+        cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(gm, lm), tm, tc, a, b)
+        mask = rp.Plan(g, cfg, 7).build_mask_device()
+        row_ptr, col_idx, order = rp.mask_to_csr(g, mask)
+        nnz = int(col_idx.numel())
+        ms = timed(lambda: rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, out=out))
+        tf = 4.0 * H * d * 128 * 128 * nnz / (ms * 1e-3) / 1e12
+        rows.append({"gamma": gm, "lambda": lm, "theta_m": tm, "theta_c": tc, "rho": [a, b],
+                     "block_sparsity": round(1 - nnz / nb / nb, 4), "nnz": nnz,
+                     "ms_per_layer": round(ms, 3), "tflops_active": round(tf, 1),
+                     "frac_of_peak": round(tf / peak, 4),
+                     "speedup_vs_ours_dense": round(dense_ms / ms, 2),
+                     "speedup_vs_sdpa": round(sdpa_ms / ms, 2)})
+    print(json.dumps({"workload": "Wan2.1-14B 21x45x80, 40 heads, d=128, bf16, B=128, 1 GPU",
+                      "peak_bf16_tflops": peak, "dense_ours_ms": round(dense_ms, 2),
+                      "dense_sdpa_ms": round(sdpa_ms, 2), "points": rows}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
