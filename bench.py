@@ -150,7 +150,46 @@ def reference_sample(cfgd, threads, target_s=20.0):
             f" on N_f=1 ({padded} padded tokens) x {heads} heads concurrently, "
             f"extrapolated x{scale:.0f} to the full layer by S'^2 * ceil(H/heads) "
             f"(the reference evaluates the expanded mask densely, O(S'^2))")
-    return dt * scale * 1e3, dt, desc, ("reference" if have_ref else "port")
+    ms = dt * scale * 1e3
+    sample_s = dt
+    if cfgd["mode"] == 1:
+        # dynamic mode also rebuilds the mask every layer: the reference's
+        # build_mask (std::thread over frame pairs, all host cores) on the
+        # first nf_s frames with H_f = 2 scoring heads, extrapolated by the
+        # ratio of token pairs scored (its own BuildTimings::scored_pairs).
+        nf_s = 5
+        gm, lm, tm, tc, a, b = cfgd["cfg"]
+        cfg = pyoracle.Cfg(1, gm, lm, 1e-6, tm, tc, a, b, 1)
+        qf, kf, _ = pyoracle.port().random_batch(nf_s * nt, 2, d, 42, with_values=False,
+                                                 threads=threads)
+        os.environ.setdefault("RADIALPLAN_THREADS", str(threads))
+        tm_ = {}
+        t1 = time.perf_counter()
+        lib.build_mask(nf_s, nt, bs, cfg, cfgd["seed"], q=qf, k=kf, timings=tm_)
+        dm = time.perf_counter() - t1
+        full_pairs = scored_pairs(lib, cfgd["nf"], nt, bs, cfg)
+        ratio = full_pairs / max(1, tm_.get("scored_pairs", 0))
+        ms += dm * ratio * 1e3
+        sample_s += dm
+        desc += (f"; plus build_mask (dynamic, {threads} threads) on N_f={nf_s} "
+                 f"({tm_.get('scored_pairs', 0)} token pairs scored, {dm:.1f} s) extrapolated "
+                 f"x{ratio:.1f} to the layer's {full_pairs} scored pairs")
+    return ms, sample_s, desc, ("reference" if have_ref else "port")
+
+
+def scored_pairs(lib, nf, nt, bs, cfg):
+    """Token pairs the reference scores in dynamic mode: the candidate bands
+    of retained frame pairs at distance >= 2 (tier 0 takes the full band
+    unscored), radial.cpp:56-62 / selection.cpp:52-59."""
+    total = 0
+    for i in range(nf):
+        for j in range(nf):
+            if abs(i - j) < 2:
+                continue
+            width, retained, count, tier, _ = lib.frame_pair(nf, nt, bs, cfg, i, j)
+            if retained and tier >= 1:
+                total += count
+    return total
 
 
 def run_reference(args, cfgd):
@@ -221,7 +260,8 @@ def main():
 
     peaks, peaks_kind = load_peaks()
     H, d = cfgd["heads"], cfgd["d"]
-    from paper_2604_20470_b200.sharding import broadcast_mask, head_shards
+    from paper_2604_20470_b200.sharding import (broadcast_scoring_features, head_shards,
+                                                or_allgather_mask)
     h0, Hl = head_shards(H, world)[rank]  # contiguous head shard per rank
     g = rp.make_grid(cfgd["nf"], cfgd["nt"], cfgd["bs"])
     gm, gl, tm, tc, a, b = cfgd["cfg"]
@@ -237,17 +277,29 @@ def main():
     stream.synchronize()
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    plan = rp.Plan(g, cfg, cfgd["seed"])
     dynamic = cfgd["mode"] == 1
+    # dynamic mode on N GPUs: split scoring (SURVEY 8e option 2) -- every rank
+    # scores 1/N of the frame pairs from a broadcast copy of the H_f = 2
+    # scoring heads, and the partial bitmasks are OR-combined
+    plan = rp.Plan(g, cfg, cfgd["seed"],
+                   rp.BuildOptions(shard_index=rank, shard_count=world) if dynamic else None)
+    score_bufs = None
+    if dynamic and world > 1:
+        score_bufs = (torch.empty((S, 2, d), dtype=torch.bfloat16, device=dev),
+                      torch.empty((S, 2, d), dtype=torch.bfloat16, device=dev))
+
+    def build_dynamic(out=None):
+        if world == 1:
+            return plan.build_mask_device(q, k, 2, out=out, stream=stream)
+        qs, ks = broadcast_scoring_features(q, k, 2, src=0, out=score_bufs)
+        m = plan.build_mask_device(qs, ks, 2, out=out, stream=stream)
+        return or_allgather_mask(m)
 
     # ---- one-time mask build (static: cached afterwards), timed -----------
     e0, e1 = ev(), ev()
     with torch.cuda.stream(stream):
         e0.record(stream)
-        mask = plan.build_mask_device(q if dynamic else None, k if dynamic else None,
-                                      2 if dynamic else 0, stream=stream)
-        if dynamic and world > 1:
-            broadcast_mask(mask, src=0)
+        mask = build_dynamic() if dynamic else plan.build_mask_device(stream=stream)
         row_ptr, col_idx, order = rp.mask_to_csr(g, mask, stream=stream)
         e1.record(stream)
     stream.synchronize()
@@ -268,12 +320,7 @@ def main():
         so its own duration feeds the roofline."""
         nonlocal row_ptr, col_idx, order
         if dynamic:
-            # the scoring heads (global 0..H_f-1) live on rank 0; it builds the
-            # mask and broadcasts the bitmask (one small NCCL collective)
-            if rank == 0:
-                plan.build_mask_device(q, k, 2, out=mask, stream=stream)
-            if world > 1:
-                broadcast_mask(mask, src=0)
+            build_dynamic(out=mask)
             row_ptr, col_idx, order = rp.mask_to_csr(g, mask, stream=stream, out=csr_bufs)
         if mark is not None:
             mark[0].record(stream)
@@ -409,7 +456,10 @@ def main():
                        "seq_len": S, "padded_tokens": g.padded_tokens,
                        "block_size": cfgd["bs"], "mask_active_blocks": nnz,
                        "block_sparsity": round(sparsity, 4),
-                       "parallelism": f"head-sharded x{world} (no data-path collective)",
+                       "parallelism": f"head-sharded x{world}" + (
+                           " (static mask cached on every rank: no collective)" if not dynamic
+                           else " (split scoring: broadcast of the 2 scoring heads + OR "
+                                "all-gather of the bitmask)" if world > 1 else ""),
                        "l2": "inputs larger than L2 (Q/K/V 2.3 GB bf16 per layer)"},
             "effective_tflops": tflops_eff,
             "algorithmic_tflops": tflops_alg,

@@ -127,7 +127,14 @@ typedef struct {
    * threshold, 2 = exact fp64 SIMT scores + sequential per-pair statistics
    * (bit-identical to the reference; for small grids and fp32 features). */
   int score_engine;
-  double recheck_delta; /* in z units; <= 0 selects the default (1e-4) */
+  double recheck_delta; /* in z units; <= 0 selects the default (1e-5) */
+  /* Multi-GPU split of the dynamic scoring (SURVEY 8e option 2): only the
+   * scored frame pairs whose ordinal (row-major over (i, j)) is congruent to
+   * shard_index mod shard_count are scored; the intra-frame rectangles and
+   * full bands are set on every shard, so the bitwise OR of all shards'
+   * masks is the unsharded mask.  Ignored in static mode.  Defaults 0 / 1. */
+  int shard_index;
+  int shard_count;
 } rp_build_options;
 
 typedef struct {

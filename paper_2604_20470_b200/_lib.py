@@ -97,6 +97,8 @@ class BuildOptions(C.Structure):
         ("disable_split", C.c_int),
         ("score_engine", C.c_int),
         ("recheck_delta", C.c_double),
+        ("shard_index", C.c_int),
+        ("shard_count", C.c_int),
     ]
 
 

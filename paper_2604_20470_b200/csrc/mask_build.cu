@@ -475,6 +475,7 @@ void make_jobs(rp_plan_s& P) {
   const rp_grid& g = P.g;
   const rp_config& c = P.c;
   const int64_t nt = g.tokens_per_frame;
+  int64_t score_ordinal = 0;
   for (int i = 0; i < g.n_frames; ++i)
     for (int j = 0; j < g.n_frames; ++j) {
       const int64_t t = std::llabs(static_cast<long long>(i) - j);
@@ -506,6 +507,9 @@ void make_jobs(rp_plan_s& P) {
                                 : (jb.tier == 1 ? c.near_param : c.far_param);
         if (jb.tier == 0) jb.kind = plan::kFullBand;
         else jb.kind = jb.n > 0 ? plan::kScore : plan::kEmpty;
+        // multi-GPU split: another shard scores this pair
+        if (jb.kind == plan::kScore && (score_ordinal++ % P.o.shard_count) != P.o.shard_index)
+          jb.kind = plan::kEmpty;
       }
       P.jobs.push_back(jb);
     }
@@ -730,6 +734,8 @@ void rp_build_options_defaults(rp_build_options* o) {
   o->disable_split = 0;
   o->score_engine = 0;
   o->recheck_delta = 0.0;
+  o->shard_index = 0;
+  o->shard_count = 1;
 }
 
 rp_status rp_plan_create(const rp_grid* g, const rp_config* c, uint64_t seed,
@@ -744,6 +750,8 @@ rp_status rp_plan_create(const rp_grid* g, const rp_config* c, uint64_t seed,
     p->seed = seed;
     if (opt) p->o = *opt;
     else rp_build_options_defaults(&p->o);
+    if (p->o.shard_count < 1 || p->o.shard_index < 0 || p->o.shard_index >= p->o.shard_count)
+      throw std::invalid_argument("build options: shard_index must be in [0, shard_count)");
     make_jobs(*p);
     p->words = static_cast<size_t>((g->blocks_per_dim * g->row_bytes + 3) / 4);
     *out = p.release();

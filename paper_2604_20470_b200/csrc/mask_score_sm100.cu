@@ -43,10 +43,13 @@ namespace rp {
 namespace mask {
 
 struct ScoreItem {
-  int32_t job;  // index into the engine's job array
-  int32_t tr;   // 128-token tile row (global)
-  int32_t tc;   // 128-token tile column (global)
-  int32_t pad;
+  int32_t job;    // index into the engine's job array
+  int32_t tr;     // 128-token tile row (global)
+  int32_t tc;     // 128-token tile column (global)
+  int32_t width;  // the job's band half-width (copied: one load per item)
+  int32_t qi;     // first token of frame i
+  int32_t kj;     // first token of frame j
+  int32_t pad0, pad1;
 };
 
 struct SParams {
@@ -60,15 +63,19 @@ struct SParams {
   const float2* job_thr;     // pass 2: (raw-unit threshold, raw-unit delta margin) per job
   uint32_t* counts;
   unsigned long long* job_kept;
-  int4* queue;
-  unsigned long long* queue_len;
-  long long queue_cap;
+  uint2* slots;          // [n_items][4 warps][kSlots]: (job, u * nt + v) to re-score
+  uint8_t* slot_cnt;     // [n_items][4 warps]
   const float* qnorm;
   const float* kmax;  // per 128-token tile: max |k'_v|
   float kappa;
   float delta_floor;
-  Feat feat;  // exact re-score in place when the recheck queue is full
+  Feat feat;  // exact re-score in place when a warp's slots overflow
 };
+
+// Undecided pairs per (item, epilogue warp) kept for the exact re-score
+// without any global atomics; more than this (never seen in practice: the
+// mean is < 1 per warp) are decided in place.
+constexpr int kSlots = 8;
 
 constexpr int kThreads = 192;  // warps 0-3 epilogue (row = thread), 4 TMA, 5 MMA
 constexpr int kChunkBytes = 128 * 128;
@@ -101,16 +108,10 @@ RP_DEV Welford chan(Welford a, Welford b) {
   return r;
 }
 
-// Undecided pair: append to the recheck queue, or -- if the queue is full --
-// decide it right here with the exact fp64 score.  Out of line so the
-// epilogue's unrolled loops stay compact.  Returns true iff kept now.
-__device__ __noinline__ bool queue_or_decide(const SParams& p, int job, const DJob& jb, int u,
-                                             int v, long long gr, long long kj, double2 st) {
-  const unsigned long long slot = atomicAdd(p.queue_len, 1ull);
-  if (slot < static_cast<unsigned long long>(p.queue_cap)) {
-    p.queue[slot] = make_int4(job, u, v, 0);
-    return false;
-  }
+// Overflowing undecided pair: decided here with the exact fp64 score.  Out
+// of line so the epilogue's unrolled loops stay compact.
+__device__ __noinline__ bool decide_exact(const SParams& p, const DJob& jb, int v, long long gr,
+                                          long long kj, double2 st) {
   return zscore(exact_score(p.feat, gr, kj + v), st) >= jb.param;
 }
 
@@ -264,12 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[buf]);
       // valid columns of this row: contiguous [c_lo, c_hi] (band + frames)
-      const long long qi = static_cast<long long>(jb.i) * p.nt;
-      const long long kj = static_cast<long long>(jb.j) * p.nt;
+      const long long qi = item.qi;
+      const long long kj = item.kj;
       const long long u = gr - qi;
       int c_lo = 1, c_hi = 0;
       if (u >= 0 && u < p.nt) {
-        const long long vlo = max(0ll, u - jb.width), vhi = min(static_cast<long long>(p.nt) - 1, u + jb.width);
+        const long long vlo = max(0ll, u - item.width), vhi = min(static_cast<long long>(p.nt) - 1, u + item.width);
         const long long g0 = static_cast<long long>(item.tc) * 128;
         c_lo = static_cast<int>(max(kj + vlo - g0, 0ll));
         c_hi = static_cast<int>(min(kj + vhi - g0, 127ll));
@@ -347,16 +348,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           kb[w4] = k1 & inm[w4];
           ub[w4] = u1 & inm[w4] & ~k1;
         }
-        // rare path: queue the undecided pairs for the exact fp64 re-score
-#pragma unroll 1
-        for (int w4 = 0; w4 < 4; ++w4) {
-          uint32_t m = ub[w4];
-          while (m) {
-            const int i = __ffs(m) - 1;
-            m &= m - 1;
-            const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 + 32 * w4 + i - kj);
-            if (queue_or_decide(p, item.job, jb, static_cast<int>(u), v, gr, kj, st))
-              kb[w4] |= 1u << i;
+        // rare path: undecided pairs go to this (item, warp)'s slots for the
+        // exact fp64 re-score (warp scan for the slot offsets, no atomics)
+        const int mine = __popc(ub[0]) + __popc(ub[1]) + __popc(ub[2]) + __popc(ub[3]);
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const long long sbase = (it * 4 + warp) * kSlots;
+        if (lane == 0) p.slot_cnt[it * 4 + warp] = static_cast<uint8_t>(min(total, kSlots));
+        if (mine) {
+          int at = incl - mine;
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            uint32_t m = ub[w4];
+            while (m) {
+              const int i = __ffs(m) - 1;
+              m &= m - 1;
+              const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 + 32 * w4 + i - kj);
+              if (at < kSlots)
+                p.slots[sbase + at] = make_uint2(static_cast<uint32_t>(item.job),
+                                                 static_cast<uint32_t>(u) * p.nt + v);
+              else if (decide_exact(p, jb, v, gr, kj, st))
+                kb[w4] |= 1u << i;
+              ++at;
+            }
           }
         }
         // per-column counts within the warp: transpose each 32 x 32 bit block
@@ -379,9 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // thread r owns column r: sum the warps of each block row
         const int bs = p.bs;
         const int rows_per_blk = bs < 128 ? bs : 128;  // bs in {32, 64, 128}
-        const int wpb = rows_per_blk / 32;             // warps per block row
+        const int wpb = rows_per_blk >> 5;             // warps per block row
         const long long gc = static_cast<long long>(item.tc) * 128 + r;
-        for (int br = 0; br < 128 / rows_per_blk; ++br) {
+        for (int br = 0; br < 4 / wpb; ++br) {
           uint32_t c2 = 0;
           for (int x = 0; x < wpb; ++x) c2 += wcnt[(br * wpb + x) * 128 + r];
           const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
@@ -459,21 +478,28 @@ __global__ void tile_max_kernel(const float* __restrict__ norms, long long token
   if (lane == 0) out[t] = m;
 }
 
-// Exact re-score of every queued pair (reference operation order).
-__global__ void recheck_kernel(const DJob* __restrict__ jobs, const int4* __restrict__ queue,
-                               const unsigned long long* __restrict__ queue_len, long long cap,
-                               Feat f, const double2* __restrict__ job_stats, uint32_t* counts,
-                               unsigned long long* job_kept, int nt, int bs) {
-  const long long n = min(static_cast<long long>(*queue_len), cap);
-  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+// Exact re-score of every undecided pair (reference operation order): one
+// thread per (item, warp) slot group.
+__global__ void recheck_kernel(const DJob* __restrict__ jobs, const uint2* __restrict__ slots,
+                               const uint8_t* __restrict__ slot_cnt, long long groups, Feat f,
+                               const double2* __restrict__ job_stats, uint32_t* counts,
+                               unsigned long long* job_kept, unsigned long long* rechecked,
+                               int nt, int bs) {
+  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < groups;
        x += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int4 e = queue[x];
-    const DJob& jb = jobs[e.x];
-    const float s = exact_score(f, static_cast<int64_t>(jb.i) * nt + e.y,
-                                static_cast<int64_t>(jb.j) * nt + e.z);
-    if (zscore(s, job_stats[e.x]) >= jb.param) {
-      add_count(jb, counts, nt, bs, e.y, e.z);
-      atomicAdd(&job_kept[e.x], 1ull);
+    const int n = slot_cnt[x];
+    if (!n) continue;
+    atomicAdd(rechecked, static_cast<unsigned long long>(n));
+    for (int e = 0; e < n; ++e) {
+      const uint2 sl = slots[x * kSlots + e];
+      const DJob& jb = jobs[sl.x];
+      const int64_t u = sl.y / nt, v = sl.y % nt;
+      const float s = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
+                                  static_cast<int64_t>(jb.j) * nt + v);
+      if (zscore(s, job_stats[sl.x]) >= jb.param) {
+        add_count(jb, counts, nt, bs, u, v);
+        atomicAdd(&job_kept[sl.x], 1ull);
+      }
     }
   }
 }
@@ -570,9 +596,9 @@ class FastEngine {
   double* d_item_stats = nullptr;
   double2* d_job_stats = nullptr;
   float2* d_job_thr = nullptr;
-  unsigned long long* d_kept = nullptr;  // [jobs + 1]: per job, then queue length
-  int4* d_queue = nullptr;
-  long long queue_cap = 0;
+  unsigned long long* d_kept = nullptr;  // [jobs + 1]: per job, then rechecked pairs
+  uint2* d_slots = nullptr;
+  uint8_t* d_slot_cnt = nullptr;
   float* d_qn = nullptr;
   float* d_kn = nullptr;
   float* d_kmax = nullptr;
@@ -583,7 +609,8 @@ class FastEngine {
                     static_cast<void*>(d_counts), static_cast<void*>(d_item_stats),
                     static_cast<void*>(d_job_stats), static_cast<void*>(d_kept),
                     static_cast<void*>(d_job_thr),
-                    static_cast<void*>(d_queue), static_cast<void*>(d_qn),
+                    static_cast<void*>(d_slots), static_cast<void*>(d_slot_cnt),
+                    static_cast<void*>(d_qn),
                     static_cast<void*>(d_kn), static_cast<void*>(d_kmax)})
       if (p) cudaFree(p);
   }
@@ -592,6 +619,8 @@ class FastEngine {
 bool fast_engine_supported(const rp_grid& g, int head_dim, int heads) {
   const int bs = g.block_size;
   if (bs != 32 && bs != 64 && bs != 128) return false;
+  if (static_cast<int64_t>(g.tokens_per_frame) * g.tokens_per_frame >= (int64_t{1} << 32))
+    return false;  // recheck slots pack u * N_t + v into 32 bits
   if (head_dim % 64 != 0 || heads < 1) return false;
   const int nc = heads * head_dim / 64;
   return nc >= 1 && nc <= 4;
@@ -634,7 +663,9 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
         const int64_t va = std::max<int64_t>(tc * 128, kj) - kj;
         const int64_t vb = std::min<int64_t>(tc * 128 + 127, kj + nt - 1) - kj;
         if (va - ub > d.width || ua - vb > d.width) continue;  // no |u - v| <= w
-        e->items.push_back(ScoreItem{job, static_cast<int32_t>(tr), static_cast<int32_t>(tc), 0});
+        e->items.push_back(ScoreItem{job, static_cast<int32_t>(tr), static_cast<int32_t>(tc),
+                                     static_cast<int32_t>(d.width), static_cast<int32_t>(qi),
+                                     static_cast<int32_t>(kj), 0, 0});
       }
     }
     for (int32_t r = 0; r < d.tr; ++r)
@@ -652,12 +683,8 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
   dalloc(&e->d_job_stats, nj);
   dalloc(&e->d_job_thr, nj);
   dalloc(&e->d_kept, nj + 1);
-  // recheck queue: 1% of the scored pairs (expected ~0.1%); pairs beyond
-  // the capacity are re-scored in place by the select pass.
-  int64_t pairs = 0;
-  for (const DJob& d : e->jobs) pairs += d.n;
-  e->queue_cap = std::min<int64_t>(std::max<int64_t>(1 << 20, pairs / 100), int64_t{1} << 27);
-  dalloc(&e->d_queue, static_cast<size_t>(e->queue_cap));
+  dalloc(&e->d_slots, e->items.size() * 4 * kSlots);
+  dalloc(&e->d_slot_cnt, e->items.size() * 4);
   dalloc(&e->d_qn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kmax, static_cast<size_t>((g.padded_tokens + 127) / 128));
@@ -737,9 +764,8 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.job_thr = e->d_job_thr;
   p.counts = e->d_counts;
   p.job_kept = e->d_kept;
-  p.queue = e->d_queue;
-  p.queue_len = e->d_kept + nj;
-  p.queue_cap = e->queue_cap;
+  p.slots = e->d_slots;
+  p.slot_cnt = e->d_slot_cnt;
   p.qnorm = e->d_qn;
   p.kmax = e->d_kmax;
   // fp32 accumulation of K = H_f * d exact bf16 products, each rounding
@@ -766,12 +792,13 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
       RP_LAUNCHED();
     }
   }
-  // exact re-score of the pairs within their error bound of tau; the
-  // queue length is read on the device (no host sync)
+  // exact re-score of the pairs within their error bound of tau
   {
-    recheck_kernel<<<sms * 8, 256, 0, s>>>(e->d_jobs, e->d_queue, e->d_kept + nj, e->queue_cap,
-                                         f, e->d_job_stats, e->d_counts, e->d_kept,
-                                         g.tokens_per_frame, g.block_size);
+    const long long groups = static_cast<long long>(e->items.size()) * 4;
+    recheck_kernel<<<static_cast<unsigned>(std::min<long long>((groups + 255) / 256, sms * 16)),
+                     256, 0, s>>>(e->d_jobs, e->d_slots, e->d_slot_cnt, groups, f,
+                                  e->d_job_stats, e->d_counts, e->d_kept, e->d_kept + nj,
+                                  g.tokens_per_frame, g.block_size);
     RP_LAUNCHED();
   }
   // fallback_k: only when it can activate a column (fallback_k >= cmin)

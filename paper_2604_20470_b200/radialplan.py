@@ -422,10 +422,13 @@ class BuildOptions:
     disable_split: bool = False
     score_engine: int = 0  # 0 auto, 1 tensor-core + fp64 recheck, 2 exact fp64
     recheck_delta: float = 0.0
+    shard_index: int = 0   # multi-GPU split of the dynamic scoring (dynrad.h)
+    shard_count: int = 1
 
     def c(self):
         return L.BuildOptions(int(self.disable_split), int(self.score_engine),
-                              float(self.recheck_delta))
+                              float(self.recheck_delta), int(self.shard_index),
+                              int(self.shard_count))
 
 
 class Plan:

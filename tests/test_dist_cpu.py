@@ -15,7 +15,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_20470_b200.sharding import broadcast_mask, gather_heads, head_shards, score_rank
+from paper_2604_20470_b200.sharding import (broadcast_mask, broadcast_scoring_features,
+                                            gather_heads, head_shards, or_allgather_mask,
+                                            score_rank)
 
 
 def test_head_shards_cover_all_heads():
@@ -78,3 +80,41 @@ def test_sharded_dynamic_layer_gloo(tmp_path, port):
     for r in range(world):
         assert np.array_equal(np.load(tmp_path / f"m{r}.npy"), mask)
         assert np.array_equal(np.load(tmp_path / f"r{r}.npy"), want)
+
+
+def _split_worker(rank, world, port, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    S, H, d, nb = 96, 4, 8, 13
+    g = torch.Generator().manual_seed(5)
+    q = torch.randn(S, H, d, generator=g) + rank  # only rank 0's copy is authoritative
+    k = torch.randn(S, H, d, generator=g) - rank
+    qs, ks = broadcast_scoring_features(q, k, 2, src=0)
+    # partial masks: common base bits + this rank's share of the scored bits
+    rng = np.random.default_rng(9)
+    base = rng.integers(0, 256, (nb, 2), dtype=np.uint8) & 0x11
+    scored = rng.integers(0, 256, (nb, 2), dtype=np.uint8) & 0xEE
+    mine = scored & (np.uint8(0x0F) if rank == 0 else np.uint8(0xF0))
+    mask = torch.from_numpy(base | mine)
+    or_allgather_mask(mask)
+    np.save(os.path.join(result_dir, f"q{rank}.npy"), qs.numpy())
+    np.save(os.path.join(result_dir, f"k{rank}.npy"), ks.numpy())
+    np.save(os.path.join(result_dir, f"m{rank}.npy"), mask.numpy())
+    np.save(os.path.join(result_dir, "want.npy"), base | scored)
+    dist.destroy_process_group()
+
+
+def test_split_scoring_exchange_gloo(tmp_path):
+    """Split dynamic scoring (SURVEY 8e option 2): the H_f scoring heads are
+    broadcast from the rank that holds them, and the per-rank partial masks
+    are OR-combined identically on every rank."""
+    world = 2
+    mp.spawn(_split_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    g = torch.Generator().manual_seed(5)
+    q = torch.randn(96, 4, 8, generator=g)
+    k = torch.randn(96, 4, 8, generator=g)
+    want = np.load(tmp_path / "want.npy")
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"q{r}.npy"), q[:, :2].numpy())
+        assert np.array_equal(np.load(tmp_path / f"k{r}.npy"), k[:, :2].numpy())
+        assert np.array_equal(np.load(tmp_path / f"m{r}.npy"), want)

@@ -130,3 +130,34 @@ def test_fast_engine_matches_reference(cuda, port, case):
     assert np.array_equal(exact, want)
     assert np.array_equal(got, want), int((got != want).sum())
     assert st["rechecked_pairs"] < 0.05 * max(st["scored_pairs"], 1)
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_split_scoring_shards_or_to_the_full_mask(cuda, engine):
+    """BuildOptions.shard_index / shard_count (multi-GPU split of the dynamic
+    scoring): the OR of every shard's mask is the unsharded mask, and the
+    shards' scored pairs partition the layer's."""
+    nf, nt, bs = (8, 256, 128) if engine == 1 else (5, 64, 16)
+    g = rp.make_grid(nf, nt, bs)
+    cfg = rp.SparsityConfig(rp.Mode.DynamicThreshold, rp.RadialParams(1.4, 0.7), 0.7, 0.45,
+                            0.05, 0.08)
+    torch.manual_seed(4)
+    q = torch.randn(g.total_tokens, 2, 64, device="cuda").to(torch.bfloat16)
+    k = torch.randn(g.total_tokens, 2, 64, device="cuda").to(torch.bfloat16)
+    st = {}
+    full = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=engine)).build_mask_device(
+        q, k, 2, stats=st)
+    for world in (2, 3):
+        acc = torch.zeros_like(full)
+        scored = 0
+        for r in range(world):
+            s2 = {}
+            part = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=engine, shard_index=r,
+                                                      shard_count=world)).build_mask_device(
+                q, k, 2, stats=s2)
+            acc |= part
+            scored += s2["scored_pairs"]
+        assert torch.equal(acc, full), world
+        assert scored == st["scored_pairs"]
+    with pytest.raises(rp.InvalidArgument):
+        rp.Plan(g, cfg, 7, rp.BuildOptions(shard_index=2, shard_count=2))
