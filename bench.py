@@ -428,6 +428,28 @@ def main():
                  "note": "full layer (all heads) dense bf16 attention on this GPU; SDPA = "
                          "torch scaled_dot_product_attention (cuDNN/flash backend)"}
 
+    # ---- the north star's pooled selector on the same Q/K -------
+    pooled = None
+    if dynamic and rank == 0:
+        with torch.cuda.stream(stream):
+            pm = torch.empty_like(mask)
+            for _ in range(2):
+                rp.pooled_select(g, cfg, q, k, 2, rp.PooledMode.Mass, 0.95, out=pm, stream=stream)
+            b0, b1 = ev(), ev()
+            b0.record(stream)
+            for _ in range(5):
+                rp.pooled_select(g, cfg, q, k, 2, rp.PooledMode.Mass, 0.95, out=pm, stream=stream)
+            b1.record(stream)
+        stream.synchronize()
+        p_ms = b0.elapsed_time(b1) / 5
+        alg = 2 * S * 2 * d * 2 + g.blocks_per_dim * g.row_bytes  # Q/K of H_f heads + mask
+        p_nnz = int(np.unpackbits(pm.cpu().numpy()).sum())
+        pooled = {"ms": p_ms, "mode": "cumulative softmax mass 0.95 over radial candidates, "
+                  "H_f=2 block-mean pooled Q/K (NOT reference semantics, SURVEY 8f1)",
+                  "algorithmic_bytes": alg, "achieved_gbs": alg / (p_ms * 1e-3) / 1e9,
+                  "hbm_frac": alg / (p_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                  "block_sparsity": round(1 - p_nnz / float(nb * nb), 4)}
+
     # ---- CPU baseline (rank 0, N=1) --------------------------------------------
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
@@ -476,6 +498,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "dense": dense or None,
+            "pooled_selector_f1": pooled,
             "stages_ms": {"attention_stage_d": float(np.mean(k6_ms)),
                           "mask_stages_a_c_plus_csr": float(np.mean(per_step) - np.mean(k6_ms))
                           if dynamic else 0.0,

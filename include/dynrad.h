@@ -217,6 +217,27 @@ rp_status rp_dynamic_select(const rp_band* band, const double* z_dev, int64_t n,
 rp_status rp_token_mask_to_blocks(const uint8_t* token_bits_dev, int64_t dim, int block_size,
                                   uint8_t* block_bits_dev, int* uniform, rp_stream stream);
 
+/* --------------------------------------------- pooled block selector --
+ * the north star's stages (b)/(c) as it words them -- NOT the
+ * reference's semantics (the reference scores every token pair of the radial
+ * band, selection.cpp:93-185; that is rp_build_mask).  Its oracle is a CPU
+ * restatement in the tests; parity against the reference is not defined.
+ *   candidates: blocks meeting the radial band |u - v| <= w(i, j) of a
+ *     retained frame pair at distance >= 2 (window / split of `c`); blocks
+ *     holding pairs at distance <= 1 are always kept (the reference's tier 0);
+ *   (b) block means of the first n_score_heads heads of Q and K (HBM-bound),
+ *     block scores Qp_r . Kp_c / sqrt(d) / n_score_heads;
+ *   (c) per block row: RP_POOLED_TOPK keeps the max(1, floor(param * n)) best
+ *     candidates; RP_POOLED_MASS keeps the smallest best-first prefix whose
+ *     softmax mass over the row's candidates reaches param; ties go to the
+ *     lower column.
+ * bf16 features, n_score_heads * head_dim <= 512.  Writes the bit-packed
+ * mask (reference layout). */
+typedef enum { RP_POOLED_TOPK = 0, RP_POOLED_MASS = 1 } rp_pooled_mode;
+rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor* q,
+                           const rp_tensor* k, int n_score_heads, int mode, double param,
+                           uint8_t* mask_bits_dev, rp_stream stream);
+
 /* -------------------------------------------------------- mask utilities --
  * Block-sparse row lists (new; the reference stops at the bitmask):
  * row_ptr[S_b+1], col_idx[col_cap] (ascending per row), row_order[S_b]

@@ -158,6 +158,8 @@ _SIGS = {
     "rp_dynamic_select": ([_P(Band), _v, C.c_int64, C.c_double, C.c_int, _v, C.c_int64,
                            _P(C.c_int64), _v], C.c_int),
     "rp_token_mask_to_blocks": ([_v, C.c_int64, C.c_int, _v, _P(C.c_int), _v], C.c_int),
+    "rp_pooled_select": ([_P(Grid), _P(Config), _P(Tensor), _P(Tensor), C.c_int, C.c_int,
+                          C.c_double, _v, _v], C.c_int),
     "rp_debug_umma_probe": ([_v, _v, _v, _v, _v, _v, _v], C.c_int),
 }
 

@@ -196,6 +196,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto load_kv = [&](const CUtensorMap* m, int h, int blk) {
         const uint32_t st = kv_it % L::kStages;
         mbar_wait(&kv_empty[st], ((kv_it / L::kStages) & 1) ^ 1);
+#ifdef RP_ABL_NOLOAD
+        // ablation (timing only): after the ring's first fill, reuse stale tiles
+        if (kv_it >= L::kStages) {
+          if (lane == 0) mbar_arrive(&kv_full[st]);
+          ++kv_it;
+          return;
+        }
+#endif
         mbar_arrive_expect_tx_w(&kv_full[st], L::kTileBytes);
         uint8_t* dst = skv + st * L::kTileBytes;
 #pragma unroll
@@ -327,75 +335,87 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_ld();
         if (tr) RP_TR2(10, g);
         auto S = [&](int e) -> float { return __uint_as_float(e < 32 ? s0[e] : s1[e - 32]); };
-        float mq[2];
+        // Row max of the two halves, combined through shared memory (slot
+        // g % 2 keeps the partner's read of this step ahead of our write two
+        // steps later).
+        auto exchange_max = [&](float mine) -> float {
+          float* slot = red_max + b * 256;
+          slot[half * 128 + r] = mine;
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+          return fmaxf(slot[r], slot[128 + r]);
+        };
+        if (j == 0) {  // first block of the unit: the reference max comes first
+          float a = S(0);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float a = S(32 * c);
-#pragma unroll
-          for (int i = 1; i < 31; i += 2) a = fmaxf(a, fmaxf(S(32 * c + i), S(32 * c + i + 1)));
-          mq[c] = fmaxf(a, S(32 * c + 31));
+          for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
+          m = exchange_max(fmaxf(a, S(63)));
         }
-        // combine the two halves' maxima of each row (slot g % 2 keeps the
-        // partner's read of this step ahead of our write two steps later)
-        float* slot = red_max + b * 256;
-        slot[half * 128 + r] = fmaxf(mq[0], mq[1]);
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
-        const float mx = fmaxf(slot[r], slot[128 + r]);
-        const float m_new = fmaxf(m, mx);
-        bool need = false;
-        float alpha = 1.0f;
-        if (j == 0) {
-          m = m_new;
-        } else if ((m_new - m) * sl2 > 8.0f) {
-          need = true;
-          alpha = ex2((m - m_new) * sl2);
-          m = m_new;
-          l *= alpha;
-        }
-        if (__any_sync(0xFFFFFFFFu, need)) {
-          // O must hold P(g-1).V(g-1) before it is rescaled
-          mbar_wait(pv_done, (g - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < D / 64; ++c) {
-            uint32_t o[32];
-            const uint32_t oc = trow + L::kO + half * (D / 2) + c * 32;
-            tmem_ld32(oc, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(oc, o);
-          }
-        }
-        // p = 2^((s - m) * scale * log2 e): 32 pairs, chunked so a chunk's
-        // exponentials overlap the packing of the previous one.
-        const float2 sc2 = make_float2(sl2, sl2);
-        const float2 ng2 = make_float2(-m * sl2, -m * sl2);
-        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        // p = 2^((s - m) * scale * log2 e) against the running reference m
+        // (stale: the max of the previous blocks, so the exponentials do not
+        // wait for this block's max).  32 pairs, chunked so a chunk's
+        // exponentials overlap the packing of the previous one; this block's
+        // max is folded in alongside and checked afterwards.
+        float2 acc[2];
         uint32_t pk[32];
-        float2 pv_prev[16];
+        float lmax = -INFINITY;
+        auto exps = [&](float mref, bool track) {
+          const float2 sc2 = make_float2(sl2, sl2);
+          const float2 ng2 = make_float2(-mref * sl2, -mref * sl2);
+          acc[0] = acc[1] = make_float2(0.f, 0.f);
+          float2 pv_prev[16];
 #pragma unroll
-        for (int c = 0; c <= 2; ++c) {
-          float2 pv_cur[16];
+          for (int c = 0; c <= 2; ++c) {
+            float2 pv_cur[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (c < 2) {
-              const int e = 32 * c + 2 * i;
-              const float2 xv = ffma2v(make_float2(S(e), S(e + 1)), sc2, ng2);
-              if (kPolyMask & (1u << (i & 7))) {
-                pv_cur[i] = ex2_poly2(xv);
-              } else {
-                pv_cur[i].x = ex2v(xv.x);
-                pv_cur[i].y = ex2v(xv.y);
+            for (int i = 0; i < 16; ++i) {
+              if (c < 2) {
+                const int e = 32 * c + 2 * i;
+                if (track) lmax = fmaxf(lmax, fmaxf(S(e), S(e + 1)));
+                const float2 xv = ffma2v(make_float2(S(e), S(e + 1)), sc2, ng2);
+                if (kPolyMask & (1u << (i & 7))) {
+                  pv_cur[i] = ex2_poly2(xv);
+                } else {
+                  pv_cur[i].x = ex2v(xv.x);
+                  pv_cur[i].y = ex2v(xv.y);
+                }
+              }
+              if (c > 0) {
+                acc[i & 1] = fadd2v(acc[i & 1], pv_prev[i]);
+                pk[16 * (c - 1) + i] = pack_bf16v(pv_prev[i].x, pv_prev[i].y);
               }
             }
-            if (c > 0) {
-              acc[i & 1] = fadd2v(acc[i & 1], pv_prev[i]);
-              pk[16 * (c - 1) + i] = pack_bf16v(pv_prev[i].x, pv_prev[i].y);
-            }
-          }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
+            for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
+          }
+        };
+        exps(m, j > 0);
+        if (j > 0) {
+          // this block's max (both halves): if it overtook the reference by
+          // more than 2^8, rebase O and l on the new max and redo the block
+          // (rare after the first blocks; exact either way)
+          const float mx = exchange_max(lmax);
+          const bool need = (mx - m) * sl2 > 8.0f;
+          if (__any_sync(0xFFFFFFFFu, need)) {
+            const float alpha = need ? ex2((m - mx) * sl2) : 1.0f;
+            if (need) {
+              m = mx;
+              l *= alpha;
+            }
+            // O must hold P(g-1).V(g-1) before it is rescaled
+            mbar_wait(pv_done, (g - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) {
+              uint32_t o[32];
+              const uint32_t oc = trow + L::kO + half * (D / 2) + c * 32;
+              tmem_ld32(oc, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(oc, o);
+            }
+            exps(m, false);
+          }
         }
         if (tr) RP_TR2(11, g);
         const float2 at = fadd2(acc[0], acc[1]);

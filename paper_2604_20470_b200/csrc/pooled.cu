@@ -1,0 +1,283 @@
+// the north star's pooled block selector -- stages (b)/(c) as
+// BASELINE.json's north_star words them, NOT the reference's semantics (the
+// reference scores every token pair of the radial band, selection.cpp:93-185;
+// its exact form is the build_mask path in mask_build.cu / mask_score_sm100.cu).
+// Its oracle is a CPU restatement in tests/test_pooled_gpu.py (parity against
+// the reference is not defined for it).
+//
+//   classify  block (r, c): forced when it holds a token pair of frames at
+//             distance t <= 1 (the reference's tier 0: intra-frame
+//             rectangles and full adjacent bands), candidate when it meets
+//             the radial band |u - v| <= w(i, j) of a retained frame pair at
+//             t >= 2 (radial.cpp:30-54 windows and split rule).
+//   pool      block means of the first H_f heads of Q and K over each block's
+//             valid tokens: one pass over 2 S H_f d bf16 -- HBM-bound,
+//             128-bit loads, fp32 accumulation, shared-memory reduction.
+//   select    one CTA per block row: s(r, c) = Qp_r . Kp_c / sqrt(d) / H_f over
+//             the candidates (warp dot products + shuffle reductions), a
+//             bitonic sort (score descending, column ascending on ties), then
+//             static-ratio top-k (keep max(1, floor(ratio n)) best) or
+//             dynamic cumulative softmax mass (smallest prefix whose softmax
+//             mass over the candidates reaches tau), and the row's bits.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+#include "plan.hpp"
+
+namespace rp {
+namespace pooled {
+
+constexpr int kMaxFeat = 512;  // H_f * d
+
+struct Dist {
+  int32_t width;
+  int32_t retained;  // frame pair at this distance survives the split rule
+};
+
+// 0 none, 1 candidate, 2 forced
+__global__ void classify_kernel(const Dist* __restrict__ tab, int nf, int64_t nt, int64_t S,
+                                int bs, int64_t nb, uint8_t* __restrict__ state) {
+  const int64_t r = blockIdx.y;
+  const int64_t t0 = r * bs, t1 = min(t0 + bs, S);  // valid query tokens [t0, t1)
+  for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nb;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k0 = c * bs, k1 = min(k0 + bs, S);
+    uint8_t st = 0;
+    if (t0 < t1 && k0 < k1) {
+      for (int64_t fi = t0 / nt; fi <= (t1 - 1) / nt; ++fi) {
+        const int64_t ua = max(t0, fi * nt) - fi * nt, ub = min(t1 - 1, fi * nt + nt - 1) - fi * nt;
+        for (int64_t fj = k0 / nt; fj <= (k1 - 1) / nt; ++fj) {
+          const int64_t va = max(k0, fj * nt) - fj * nt, vb = min(k1 - 1, fj * nt + nt - 1) - fj * nt;
+          const int64_t t = fi > fj ? fi - fj : fj - fi;
+          if (t <= 1) {
+            st = 2;
+          } else if (tab[t].retained && !(va - ub > tab[t].width || ua - vb > tab[t].width)) {
+            if (st == 0) st = 1;
+          }
+        }
+      }
+    }
+    state[r * nb + c] = st;
+  }
+}
+
+// Block means of the first `heads` heads (H_f * d <= 512 values per token).
+// blockIdx.x = block, blockIdx.y = 0 (Q) / 1 (K).  256 threads: 32 chunks of
+// 8 values (one 16-byte load each) x 8 token groups.
+__global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restrict__ q,
+                                                   const __nv_bfloat16* __restrict__ k,
+                                                   int64_t ts, int64_t hs, int heads, int d,
+                                                   int64_t S, int bs, float* __restrict__ qp,
+                                                   float* __restrict__ kp) {
+  const __nv_bfloat16* x = blockIdx.y ? k : q;
+  float* out = blockIdx.y ? kp : qp;
+  const int64_t b = blockIdx.x;
+  const int64_t t0 = b * bs, t1 = min(t0 + bs, S);
+  const int F = heads * d, chunks = F / 8;
+  __shared__ float red[8][kMaxFeat];
+  const int grp = threadIdx.x / 32;
+  for (int ch = threadIdx.x % 32; ch < chunks; ch += 32) {
+    const int h = (ch * 8) / d, e = (ch * 8) % d;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int64_t t = t0 + grp; t < t1; t += 8) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + t * ts + h * hs + e));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] += __uint_as_float(w[i] << 16);
+        acc[2 * i + 1] += __uint_as_float(w[i] & 0xFFFF0000u);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[grp][ch * 8 + i] = acc[i];
+  }
+  __syncthreads();
+  const float inv = t1 > t0 ? 1.f / static_cast<float>(t1 - t0) : 0.f;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) s += red[g][f];
+    out[b * F + f] = s * inv;
+  }
+}
+
+// One CTA (256 threads) per block row.  Dynamic shared memory: the row's
+// pooled query (F floats), then cap (score, column) pairs, cap a power of two
+// >= the block count.
+__global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ qp,
+                                                     const float* __restrict__ kp, int F,
+                                                     float scale, const uint8_t* __restrict__ state,
+                                                     int64_t nb, int64_t row_bytes, int cap,
+                                                     int mode, double param,
+                                                     uint8_t* __restrict__ bits) {
+  extern __shared__ float sm[];
+  float* qrow = sm;                                   // [F]
+  float* sc = sm + F;                                 // [cap]
+  int* ci = reinterpret_cast<int*>(sc + cap);         // [cap]
+  uint32_t* words = reinterpret_cast<uint32_t*>(ci + cap);  // [row_bytes/4 + 1]
+  __shared__ int n_cand;
+  __shared__ int n_keep;
+  const int64_t r = blockIdx.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) qrow[f] = qp[r * F + f];
+  const int nwords = static_cast<int>((row_bytes + 3) / 4);
+  for (int w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0u;
+  if (threadIdx.x == 0) n_cand = 0;
+  __syncthreads();
+  // candidate scores (warp per column), forced bits
+  for (int64_t c = warp; c < nb; c += blockDim.x / 32) {
+    const uint8_t st = state[r * nb + c];
+    if (st == 2 && lane == 0) atomicOr(&words[c / 32], 1u << (c % 32));
+    if (st != 1) continue;
+    float acc = 0.f;
+    for (int f = lane; f < F; f += 32) acc = fmaf(qrow[f], __ldg(kp + c * F + f), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0) {
+      const int at = atomicAdd(&n_cand, 1);
+      sc[at] = acc * scale;
+      ci[at] = static_cast<int>(c);
+    }
+  }
+  __syncthreads();
+  const int n = n_cand;
+  for (int i = n + threadIdx.x; i < cap; i += blockDim.x) {
+    sc[i] = -INFINITY;
+    ci[i] = 0x7FFFFFFF;
+  }
+  __syncthreads();
+  // bitonic sort: score descending, column ascending
+  for (int size = 2; size <= cap; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < cap / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const float a = sc[lo], bb = sc[hi];
+        const int ia = ci[lo], ib = ci[hi];
+        const bool a_first = a > bb || (a == bb && ia < ib);
+        if (a_first != desc) {
+          sc[lo] = bb;
+          sc[hi] = a;
+          ci[lo] = ib;
+          ci[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    int keep = 0;
+    if (n > 0) {
+      if (mode == RP_POOLED_TOPK) {
+        keep = static_cast<int>(floor(static_cast<double>(n) * param));
+        keep = keep < 1 ? 1 : keep;
+      } else {
+        // smallest prefix whose softmax mass reaches tau (fp64, in order)
+        const double mx = sc[0];
+        double total = 0.0;
+        for (int i = 0; i < n; ++i) total += exp(static_cast<double>(sc[i]) - mx);
+        double run = 0.0;
+        keep = n;
+        for (int i = 0; i < n; ++i) {
+          run += exp(static_cast<double>(sc[i]) - mx);
+          if (run >= param * total) {
+            keep = i + 1;
+            break;
+          }
+        }
+      }
+    }
+    n_keep = keep;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_keep; i += blockDim.x) atomicOr(&words[ci[i] / 32], 1u << (ci[i] % 32));
+  __syncthreads();
+  uint8_t* row = bits + r * row_bytes;
+  for (int64_t x = threadIdx.x; x < row_bytes; x += blockDim.x)
+    row[x] = static_cast<uint8_t>(words[x / 4] >> (8 * (x % 4)));
+}
+
+}  // namespace pooled
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor* q,
+                           const rp_tensor* k, int n_score_heads, int mode, double param,
+                           uint8_t* mask_bits_dev, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    if (!c) throw std::invalid_argument("config: null");
+    if (!q || !k || !q->data || !k->data || q->dtype != RP_BF16 || k->dtype != RP_BF16)
+      throw std::invalid_argument("pooled select: bf16 features required");
+    if (n_score_heads < 1 || n_score_heads > q->heads || q->heads != k->heads ||
+        q->head_dim != k->head_dim || q->head_stride != k->head_stride ||
+        q->token_stride != k->token_stride)
+      throw std::invalid_argument("feature batch: queries/keys shape mismatch");
+    const int F = n_score_heads * q->head_dim;
+    if (F > pooled::kMaxFeat || q->head_dim % 8 || q->head_stride % 8 || q->token_stride % 8)
+      throw std::invalid_argument("pooled select: H_f * d <= 512, 16-byte aligned rows");
+    if (q->tokens < g->total_tokens || k->tokens < g->total_tokens)
+      throw std::invalid_argument("build_mask: feature batch too short");
+    if (mode == RP_POOLED_TOPK ? !(param > 0.0 && param <= 1.0) : !(param > 0.0 && param <= 1.0))
+      throw std::invalid_argument("pooled select: ratio / mass must be in (0, 1]");
+    if (mode != RP_POOLED_TOPK && mode != RP_POOLED_MASS)
+      throw std::invalid_argument("pooled select: unknown mode");
+    if (!mask_bits_dev) throw std::invalid_argument("build_mask: null mask buffer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nb = g->blocks_per_dim;
+    int cap = 2;
+    while (cap < nb) cap <<= 1;
+    const size_t smem = static_cast<size_t>(F) * 4 + static_cast<size_t>(cap) * 8 +
+                        static_cast<size_t>((g->row_bytes + 3) / 4 + 1) * 4;
+    if (smem > 200 * 1024) throw std::invalid_argument("pooled select: grid too large");
+    // per-distance window and split decisions (radial.cpp:30-54)
+    std::vector<pooled::Dist> tab(static_cast<size_t>(g->n_frames));
+    for (int t = 0; t < g->n_frames; ++t) {
+      tab[t].width = static_cast<int32_t>(plan::window_width(0, t, *c, *g));
+      tab[t].retained = plan::frame_retained(t, *c, *g) ? 1 : 0;
+    }
+    pooled::Dist* d_tab = nullptr;
+    uint8_t* d_state = nullptr;
+    float *d_qp = nullptr, *d_kp = nullptr;
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), sizeof(pooled::Dist) * tab.size(), s));
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_state), static_cast<size_t>(nb * nb), s));
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_qp), sizeof(float) * nb * F, s));
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_kp), sizeof(float) * nb * F, s));
+    RP_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(pooled::Dist) * tab.size(),
+                            cudaMemcpyHostToDevice, s));
+    pooled::classify_kernel<<<dim3(static_cast<unsigned>((nb + 255) / 256),
+                                   static_cast<unsigned>(nb)), 256, 0, s>>>(
+        d_tab, g->n_frames, g->tokens_per_frame, g->total_tokens, g->block_size, nb, d_state);
+    RP_LAUNCHED();
+    pooled::pool_kernel<<<dim3(static_cast<unsigned>(nb), 2), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(q->data), static_cast<const __nv_bfloat16*>(k->data),
+        q->token_stride, q->head_stride, n_score_heads, q->head_dim, g->total_tokens,
+        g->block_size, d_qp, d_kp);
+    RP_LAUNCHED();
+    static bool attr = false;
+    if (!attr) {
+      RP_CUDA(cudaFuncSetAttribute(pooled::select_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(q->head_dim)) /
+                                           n_score_heads);
+    pooled::select_kernel<<<static_cast<unsigned>(nb), 256, smem, s>>>(
+        d_qp, d_kp, F, scale, d_state, nb, g->row_bytes, cap, mode, param, mask_bits_dev);
+    RP_LAUNCHED();
+    RP_CUDA(cudaFreeAsync(d_tab, s));
+    RP_CUDA(cudaFreeAsync(d_state, s));
+    RP_CUDA(cudaFreeAsync(d_qp, s));
+    RP_CUDA(cudaFreeAsync(d_kp, s));
+  });
+}
+
+}  // extern "C"

@@ -589,5 +589,26 @@ def masked_attention_exact(g: GridSpec, mask: BlockMask, q: np.ndarray, k: np.nd
     return out
 
 
+class PooledMode(enum.IntEnum):
+    TopK = 0   # static ratio: keep max(1, floor(ratio * n)) best candidates per block row
+    Mass = 1   # dynamic: smallest best-first prefix reaching a softmax mass
+
+
+def pooled_select(g: GridSpec, c: SparsityConfig, q, k, n_score_heads: int, mode: PooledMode,
+                  param: float, out=None, stream=None):
+    """SURVEY 8(f1), the north star's pooled selector (rp_pooled_select): NOT
+    the reference's token-pair semantics.  q/k bf16 [tokens, heads, d] on the
+    GPU; returns the bit-packed block mask [S_b, row_bytes] uint8."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((g.blocks_per_dim, g.row_bytes), dtype=torch.uint8, device="cuda")
+    gc, cc = g.c(), c.c()
+    tq, tk = _tensor(q), _tensor(k)
+    L.check(L.lib().rp_pooled_select(C.byref(gc), C.byref(cc), C.byref(tq), C.byref(tk),
+                                     int(n_score_heads), int(mode), float(param),
+                                     C.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
+
+
 def kernel_launch_count() -> int:
     return int(L.lib().rp_kernel_launch_count())

@@ -10,5 +10,5 @@ mkdir -p $ROOT/variants $B/var
 [ -f $B/mask_build.o ] && [ -f $B/mask_score_sm100.o ] || make -s -C $C >/dev/null
 nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
   -I$ROOT/include -I$C --expt-relaxed-constexpr -Xptxas -v $2 -c -o $B/var/$1.o $C/capi.cu 2> $B/var/$1.log
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/variants/$1.so $B/var/$1.o $B/mask_build.o $B/mask_score_sm100.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/variants/$1.so $B/var/$1.o $(ls $B/*.o | grep -v "/capi.o")
 grep -A1 "bsfa_fwd_kernelILi128" $B/var/$1.log | grep -o "Used [0-9]* registers.*" | head -1
