@@ -20,6 +20,7 @@
 #include "attn_f32.cu"
 #include "attn_sm100.cu"
 #include "attn_sm100_db.cu"
+#include "attn_sm100_rp.cu"
 #include "csr.cu"
 
 namespace rp {
@@ -66,14 +67,20 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (t->token_stride % 8 || t->head_stride % 8)
         throw std::invalid_argument("sparse attention (bf16): strides must be multiples of 8");
     const CUtensorMap mq = make_map_bf16(q), mk = make_map_bf16(k), mv = make_map_bf16(v);
-    // K6 variant: "db" (default) = one query tile per CTA with the score
-    // tile double-buffered in TMEM (attn_sm100_db.cu); "pair" = two-head
-    // ping-pong (attn_sm100.cu), kept for comparison (DYNRAD_K6=pair).
-    static const bool pair_kernel = [] {
+    // K6 variant (DYNRAD_K6): "db" (default) = one query tile per CTA,
+    // score tile double-buffered in TMEM (attn_sm100_db.cu); "rp" = block-row
+    // pairs of one head sharing every K/V tile (attn_sm100_rp.cu: fastest on
+    // dense / long shared lists, 69 % of peak dense, on par on radial
+    // masks); "pair" = two heads of one block row ping-ponging
+    // (attn_sm100.cu).  Measured side by side in DESIGN.md section 8.
+    static const int variant = [] {
       const char* e = std::getenv("DYNRAD_K6");
-      return e && std::strcmp(e, "pair") == 0;
+      if (e && std::strcmp(e, "pair") == 0) return 2;
+      if (e && std::strcmp(e, "rp") == 0) return 0;
+      return 1;
     }();
-    // Both kernels re-balance registers between warpgroups with setmaxnreg;
+    const bool pair_kernel = variant == 2;
+    // The kernels re-balance registers between warpgroups with setmaxnreg;
     // that only works if the launch allocates the full 168 x 384 pool.
     auto check_regs = [](const void* fn) {
       cudaFuncAttributes fa;
@@ -87,6 +94,62 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       done = true;
     };
+    if (variant == 0) {
+      // union block lists of the row pairs (2p, 2p+1), LPT order
+      const int n_rows = static_cast<int>(g.blocks_per_dim);
+      const int n_pairs = (n_rows + 1) / 2;
+      const size_t cap = static_cast<size_t>(n_pairs) * n_rows;
+      int32_t *pcnt = nullptr, *prow = nullptr, *pcol = nullptr, *pord = nullptr;
+      uint8_t* pflag = nullptr;
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcnt), sizeof(int32_t) * (n_pairs + 1), stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prow), sizeof(int32_t) * (n_pairs + 1), stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcol), sizeof(int32_t) * cap, stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pflag), cap, stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pord), sizeof(int32_t) * n_pairs, stream));
+      const unsigned pg = static_cast<unsigned>((n_pairs + 127) / 128);
+      attn3::pair_count_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, pcnt);
+      RP_LAUNCHED();
+      csr::scan_kernel<<<1, 1024, 0, stream>>>(pcnt, n_pairs, prow, nullptr);
+      RP_LAUNCHED();
+      attn3::pair_fill_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, prow,
+                                                     pcol, pflag);
+      RP_LAUNCHED();
+      csr::order_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, stream>>>(
+          pcnt, n_pairs, pord);
+      RP_LAUNCHED();
+      attn3::Params p;
+      p.row_ptr = row_ptr;
+      p.prow_ptr = prow;
+      p.pcol = pcol;
+      p.pflag = pflag;
+      p.porder = pord;
+      p.n_rows = n_rows;
+      p.n_pairs = n_pairs;
+      p.heads = q.heads;
+      p.n_units = static_cast<long long>(q.heads) * n_pairs;
+      p.out = static_cast<__nv_bfloat16*>(o.data);
+      p.out_tok_stride = o.token_stride;
+      p.out_head_stride = o.head_stride;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
+      if (d == 128) {
+        static bool done = false;
+        const int smem = attn3::Layout<128>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128>), smem, done);
+        attn3::bsfa_fwd_rp_kernel<128><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv, p);
+      } else {
+        static bool done = false;
+        const int smem = attn3::Layout<64>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<64>), smem, done);
+        attn3::bsfa_fwd_rp_kernel<64><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv, p);
+      }
+      RP_LAUNCHED();
+      for (void* ptr : {static_cast<void*>(pcnt), static_cast<void*>(prow),
+                        static_cast<void*>(pcol), static_cast<void*>(pflag),
+                        static_cast<void*>(pord)})
+        RP_CUDA(cudaFreeAsync(ptr, stream));
+      return;
+    }
     if (!pair_kernel) {
       attn2::Params p;
       p.row_ptr = row_ptr;

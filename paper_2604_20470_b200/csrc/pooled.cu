@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ q
   uint32_t* words = reinterpret_cast<uint32_t*>(ci + cap);  // [row_bytes/4 + 1]
   __shared__ int n_cand;
   __shared__ int n_keep;
+  __shared__ double red_total;
   const int64_t r = blockIdx.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int f = threadIdx.x; f < F; f += blockDim.x) qrow[f] = qp[r * F + f];
@@ -169,29 +170,42 @@ __global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ q
       __syncthreads();
     }
   }
-  if (threadIdx.x == 0) {
-    int keep = 0;
-    if (n > 0) {
-      if (mode == RP_POOLED_TOPK) {
-        keep = static_cast<int>(floor(static_cast<double>(n) * param));
-        keep = keep < 1 ? 1 : keep;
-      } else {
-        // smallest prefix whose softmax mass reaches tau (fp64, in order)
-        const double mx = sc[0];
-        double total = 0.0;
-        for (int i = 0; i < n; ++i) total += exp(static_cast<double>(sc[i]) - mx);
-        double run = 0.0;
-        keep = n;
-        for (int i = 0; i < n; ++i) {
-          run += exp(static_cast<double>(sc[i]) - mx);
-          if (run >= param * total) {
-            keep = i + 1;
-            break;
-          }
-        }
+  if (mode == RP_POOLED_TOPK) {
+    if (threadIdx.x == 0) {
+      int keep = n > 0 ? static_cast<int>(floor(static_cast<double>(n) * param)) : 0;
+      n_keep = n > 0 && keep < 1 ? 1 : keep;
+    }
+  } else {
+    // smallest best-first prefix whose softmax mass reaches param: weights
+    // in fp64, a segmented block scan (thread t owns a contiguous segment)
+    __shared__ double seg[256];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+    const double mx = n > 0 ? static_cast<double>(sc[0]) : 0.0;
+    double part = 0.0;
+    for (int i = b0; i < b1; ++i) part += exp(static_cast<double>(sc[i]) - mx);
+    seg[threadIdx.x] = part;
+    if (threadIdx.x == 0) n_keep = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // 256 segment sums: sequential exclusive scan
+      double run = 0.0;
+      for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {
+        const double v = seg[t];
+        seg[t] = run;
+        run += v;
+      }
+      red_total = run;
+    }
+    __syncthreads();
+    const double target = param * red_total;
+    double run = seg[threadIdx.x];
+    for (int i = b0; i < b1; ++i) {
+      run += exp(static_cast<double>(sc[i]) - mx);
+      if (run >= target) {
+        atomicMin(&n_keep, i + 1);
+        break;
       }
     }
-    n_keep = keep;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_keep; i += blockDim.x) atomicOr(&words[ci[i] / 32], 1u << (ci[i] % 32));
