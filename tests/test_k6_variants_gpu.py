@@ -1,0 +1,23 @@
+"""The alternative stage-(d) kernels (DYNRAD_K6=rp: block-row pairs sharing
+K/V over union lists; DYNRAD_K6=pair: two-head ping-pong) pass the same bf16
+parity tests as the default kernel.  The variant is fixed per process, so each
+runs the attention test module in a subprocess."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("variant", ["rp", "pair"])
+def test_variant_passes_attention_parity(cuda, variant):
+    env = dict(os.environ, DYNRAD_K6=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_attention_gpu.py"),
+                        "-k", "bf16 or wan_shape or empty_row or host_pipeline"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
