@@ -459,10 +459,9 @@ def main():
                "sample": desc, "sample_wall_s": dt}
 
     traffic = None
-    pair = os.environ.get("DYNRAD_K6") == "pair"
-    kname = "bsfa_fwd_kernel<128> (two-head ping-pong)" if pair else "bsfa_fwd_db_kernel<128>"
-    prof = os.path.join(ROOT, "profiles", "k6pair_ncu_summary.json" if pair else
-                        "k6db_ncu_summary.json")
+    rpk = os.environ.get("DYNRAD_K6") == "rp"
+    kname = "bsfa_fwd_rp_kernel<128> (row pairs)" if rpk else "bsfa_fwd_db_kernel<128>"
+    prof = os.path.join(ROOT, "profiles", "k6db_ncu_summary.json")
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")

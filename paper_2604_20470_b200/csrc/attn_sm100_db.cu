@@ -53,11 +53,16 @@ struct Layout {
   static constexpr int kStages = D == 128 ? 4 : 8;  // 2 Q tiles + ring <= 227 KB
 #endif
   static constexpr int kSmemData = 2 * kTileBytes + kStages * kTileBytes;
-  static constexpr int kNumBars = 2 * kStages + 13;
+  static constexpr int kNumBars = 2 * kStages + 13 + 2;
   static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128) * 4;  // row max x2 slots, row sums
   static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + kRedBytes + 1024;
   static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory");
   static constexpr uint32_t kO = 256;  // TMEM column of O
+  // Q tiles as the A operand of S = Q K^T live in TMEM (bf16 pairs, D/2
+  // columns each, double-buffered by unit): the tensor core then reads only
+  // K from shared memory for S, which cuts the step's shared-memory traffic
+  // (Q 32 KB + K 32 KB + V 32 KB reads + 64 KB TMA writes) by a fifth.
+  RP_HD static uint32_t qt_col(int b) { return 384u + (b ? 64u : 0u); }
 };
 
 struct Params {
@@ -151,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* pv_done = q_full + 8;            // MMA -> softmax: a P.V retired
   uint64_t* o_done = q_full + 9;             // MMA -> softmax: unit's last P.V retired
   uint64_t* o_free = q_full + 10;            // softmax -> MMA: epilogue read O (8 warps)
+  uint64_t* qt_full = q_full + 11;           // [2] softmax -> MMA: Q in TMEM (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
   float* red_max = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 halves][128]
   float* red_l = red_max + 2 * 2 * 128;                       // [2 halves][128]
@@ -165,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(&q_full[x], 1);
-      mbar_init(&q_empty[x], 1);
+      mbar_init(&q_empty[x], 8);  // the softmax warps release Q after copying it to TMEM
+      mbar_init(&qt_full[x], 8);
       mbar_init(&s_full[x], 1);
       mbar_init(&p_full[x], 8);
     }
@@ -238,7 +245,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ----------------------------------------------------- MMA issuer ---
       const uint32_t idesc_qk = idesc_bf16(128, 128, false, false);
       const uint32_t idesc_pv = idesc_bf16(128, D, false, true);
-      const uint32_t sq_addr = smem_u32(sq);
       const uint32_t skv_addr = smem_u32(skv);
       uint32_t kv_it = 0, gs = 0, gp = 0;
       Cursor cs, cp;
@@ -247,22 +253,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       // S(gs) = Q . K(gs)^T into buffer gs % 2 (128 x 128, K = D).
       auto issue_s = [&]() {
         const int qb = cs.ord & 1;
-        if (cs.j == 0) mbar_wait(&q_full[qb], (cs.ord >> 1) & 1);
+        if (cs.j == 0) mbar_wait(&qt_full[qb], (cs.ord >> 1) & 1);
         const uint32_t st = kv_it % L::kStages;
         mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
         tc_fence_after();
-        const uint32_t qa = sq_addr + qb * L::kTileBytes;
         const uint32_t kb = skv_addr + st * L::kTileBytes;
         const uint32_t dst = tmem + (gs & 1) * 128;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk / 4) * L::kChunkBytes + (kk % 4) * 32;
-          umma_ss_w(dst, smem_desc_sw128(qa + off, 0, 1024), smem_desc_sw128(kb + off, 0, 1024),
+          umma_ts_w(dst, tmem + L::qt_col(qb) + kk * 8, smem_desc_sw128(kb + off, 0, 1024),
                     idesc_qk, kk > 0);
         }
         umma_commit_w(&kv_empty[st]);
         umma_commit_w(&s_full[gs & 1]);
-        if (cs.j == cs.n - 1) umma_commit_w(&q_empty[qb]);
         ++kv_it;
         ++gs;
         cs.next(p);
@@ -306,6 +310,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tr = lane == 0 && wq == 0 && half == 0;
     uint32_t g = 0;
     int ord = 0;
+    // Copy the Q tile of non-empty unit `o` (shared-memory buffer o % 2,
+    // 128B-swizzled by TMA) into its TMEM buffer: this thread's row, half of
+    // the head dimension, bf16 pairs -- the layout P uses as an A operand.
+    auto q_to_tmem = [&](int o) {
+      const int qb = o & 1;
+      mbar_wait(&q_full[qb], (o >> 1) & 1);
+      constexpr int kUnits = D / 16;  // 16-byte units per half row
+      uint32_t v[2 * kUnits * 2];
+      const uint8_t* base = sq + qb * L::kTileBytes + r * 128;
+#pragma unroll
+      for (int t = 0; t < kUnits; ++t) {
+        const int unit = half * kUnits + t;  // along the row
+        const int chunk = unit / 8, uu = unit % 8;
+        const uint4 x = *reinterpret_cast<const uint4*>(base + chunk * L::kChunkBytes +
+                                                         ((uu ^ (r & 7)) * 16));
+        v[4 * t + 0] = x.x;
+        v[4 * t + 1] = x.y;
+        v[4 * t + 2] = x.z;
+        v[4 * t + 3] = x.w;
+      }
+      if constexpr (D == 128) {
+        tmem_st32(trow + L::qt_col(qb) + half * 32, *reinterpret_cast<const uint32_t(*)[32]>(v));
+      } else {
+        tmem_st16(trow + L::qt_col(qb) + half * 16, v);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&qt_full[qb]);
+        mbar_arrive(&q_empty[qb]);  // the shared-memory copy is free again
+      }
+    };
+    // Non-empty units of this CTA, in order (the producer / MMA Cursor skips
+    // empty rows the same way).
+    auto next_nonempty = [&](long long u) -> long long {
+      for (; u < p.n_units; u += gridDim.x) {
+        const int ri = static_cast<int>(u % p.n_rows);
+        const int row = p.row_order ? __ldg(p.row_order + ri) : ri;
+        if (__ldg(p.row_ptr + row + 1) > __ldg(p.row_ptr + row)) return u;
+      }
+      return p.n_units;
+    };
+    long long nx = next_nonempty(blockIdx.x);
+    if (nx < p.n_units) q_to_tmem(0);
     for (long long u = blockIdx.x; u < p.n_units; u += gridDim.x) {
       const int h = static_cast<int>(u / p.n_rows);
       const int ri = static_cast<int>(u % p.n_rows);
@@ -427,6 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[b]);
         if (tr) RP_TR2(2, g);
       }
+      // the next unit's Q goes to TMEM before this unit's epilogue: the MMA
+      // warp issues the next unit's first S ahead of this unit's last P.V
+      if (next_nonempty(u + gridDim.x) < p.n_units) q_to_tmem(ord + 1);
       // epilogue: wait for the unit's last P.V, combine the halves' sums,
       // O / l -> bf16 -> global (this half's D/2 columns)
       red_l[half * 128 + r] = l;

@@ -18,7 +18,7 @@
 // Pull in the kernel definitions (single translation unit keeps template
 // instantiation and the launch sites together).
 #include "attn_f32.cu"
-#include "attn_sm100.cu"
+#include "umma_probe.cu"
 #include "attn_sm100_db.cu"
 #include "attn_sm100_rp.cu"
 #include "csr.cu"
@@ -68,24 +68,21 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
         throw std::invalid_argument("sparse attention (bf16): strides must be multiples of 8");
     const CUtensorMap mq = make_map_bf16(q), mk = make_map_bf16(k), mv = make_map_bf16(v);
     // K6 variant (DYNRAD_K6): "db" (default) = one query tile per CTA,
-    // score tile double-buffered in TMEM (attn_sm100_db.cu); "rp" = block-row
-    // pairs of one head sharing every K/V tile (attn_sm100_rp.cu: fastest on
-    // dense / long shared lists, 69 % of peak dense, on par on radial
-    // masks); "pair" = two heads of one block row ping-ponging
-    // (attn_sm100.cu).  Measured side by side in DESIGN.md section 8.
+    // score tile double-buffered in TMEM, Q in TMEM (attn_sm100_db.cu);
+    // "rp" = block-row pairs of one head sharing every K/V tile
+    // (attn_sm100_rp.cu: fastest on dense / long shared lists).  Measured side
+    // by side in DESIGN.md section 8.
     static const int variant = [] {
       const char* e = std::getenv("DYNRAD_K6");
-      if (e && std::strcmp(e, "pair") == 0) return 2;
       if (e && std::strcmp(e, "rp") == 0) return 0;
       return 1;
     }();
-    const bool pair_kernel = variant == 2;
     // The kernels re-balance registers between warpgroups with setmaxnreg;
     // that only works if the launch allocates the full 168 x 384 pool.
     auto check_regs = [](const void* fn) {
       cudaFuncAttributes fa;
       RP_CUDA(cudaFuncGetAttributes(&fa, fn));
-      if (fa.numRegs * attn::kThreads < 2 * 128 * 208 + 128 * 88)
+      if (fa.numRegs * attn2::kThreads < 2 * 128 * 208 + 128 * 88)
         throw CudaError("K6 compiled with too few registers for its setmaxnreg plan");
     };
     auto prepare = [&](const void* fn, int smem, bool& done) {
@@ -150,7 +147,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
         RP_CUDA(cudaFreeAsync(ptr, stream));
       return;
     }
-    if (!pair_kernel) {
+    {
       attn2::Params p;
       p.row_ptr = row_ptr;
       p.col_idx = col_idx;
@@ -177,31 +174,6 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_LAUNCHED();
       return;
     }
-    attn::Params p;
-    p.row_ptr = row_ptr;
-    p.col_idx = col_idx;
-    p.row_order = row_order;
-    p.n_rows = static_cast<int>(g.blocks_per_dim);
-    p.heads = q.heads;
-    p.n_pairs = (q.heads + 1) / 2;
-    p.n_units = static_cast<long long>(p.n_pairs) * p.n_rows;
-    p.out = static_cast<__nv_bfloat16*>(o.data);
-    p.out_tok_stride = o.token_stride;
-    p.out_head_stride = o.head_stride;
-    p.scale_log2 = scale * 1.4426950408889634f;
-    const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-    if (d == 128) {
-      static bool done = false;
-      const int smem = attn::Layout<128>::kSmemBytes;
-      prepare(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<128>), smem, done);
-      attn::bsfa_fwd_kernel<128><<<grid, attn::kThreads, smem, stream>>>(mq, mk, mv, p);
-    } else {
-      static bool done = false;
-      const int smem = attn::Layout<64>::kSmemBytes;
-      prepare(reinterpret_cast<const void*>(attn::bsfa_fwd_kernel<64>), smem, done);
-      attn::bsfa_fwd_kernel<64><<<grid, attn::kThreads, smem, stream>>>(mq, mk, mv, p);
-    }
-    RP_LAUNCHED();
   } else {
     if (d > attn32::kMaxD)
       throw std::invalid_argument("sparse attention (f32): head_dim must be <= 128");
@@ -300,9 +272,6 @@ const char* rp_version(void) { return "dynrad-b200 0.1 (sm_100a)"; }
 int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
 #ifdef RP_TRACE
 int rp_debug_trace(void* host) {
-  const char* e = std::getenv("DYNRAD_K6");
-  if (e && std::strcmp(e, "pair") == 0)
-    return cudaMemcpyFromSymbol(host, attn::g_trace, sizeof(attn::g_trace)) == cudaSuccess ? 0 : 1;
   return cudaMemcpyFromSymbol(host, attn2::g_trace, sizeof(attn2::g_trace)) == cudaSuccess ? 0 : 1;
 }
 #endif
