@@ -155,6 +155,8 @@ class _RefLib(_Lib):
         L.ref_proxy_scores.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
                                        _f32p, _f32p, C.c_int64, C.c_int, C.c_int, _f32p,
                                        _P(C.c_double), _P(C.c_double)]
+        L.ref_write_mask.argtypes = [_u8p, C.c_int64, C.c_int, C.c_char_p]
+        L.ref_read_mask.argtypes = [C.c_char_p, _u8p, C.c_int64, _P(C.c_int64)]
         L.ref_dynamic_select.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
                                          _P(C.c_double), C.c_int64, C.c_double, C.c_int,
                                          _P(C.c_int64), C.c_int64, _P(C.c_int64)]
@@ -236,6 +238,18 @@ class _RefLib(_Lib):
                                             h, d, _fp(s), z.ctypes.data_as(_P(C.c_double)),
                                             st))
         return s[:n], z[:n], (st[0], st[1])
+
+    def write_mask(self, bits, dim, fmt, path):
+        bits = np.ascontiguousarray(bits, np.uint8)
+        self._chk(self.lib.ref_write_mask(bits.ctypes.data_as(_u8p), dim, fmt, path.encode()))
+
+    def read_mask(self, path, cap=1 << 26):
+        buf = np.zeros(cap, np.uint8)
+        dim = C.c_int64()
+        self._chk(self.lib.ref_read_mask(path.encode(), buf.ctypes.data_as(_u8p), cap,
+                                         C.byref(dim)))
+        rb = (dim.value + 7) // 8
+        return dim.value, buf[: dim.value * rb].reshape(dim.value, rb).copy()
 
     def dynamic_select(self, nf, nt, bs, cfg: Cfg, i, j, z, tau, fallback_k):
         z = np.ascontiguousarray(z, np.float64)

@@ -289,4 +289,26 @@ int ref_dynamic_select(int nf, int nt, int bs, const ref_cfg* cfg, int i, int j,
   });
 }
 
+// write_mask / read_mask (mask.cpp:291-376): the reference's own mask files.
+// fmt: 0 binary (DRBM), 1 CSV, 2 PGM.
+int ref_write_mask(const std::uint8_t* bits, std::int64_t dim, int fmt, const char* path) {
+  return guarded([&] {
+    BlockMask m(dim);
+    std::memcpy(m.bits.data(), bits, m.bits.size());
+    write_mask(m, fmt == 0 ? MaskFormat::Binary : fmt == 1 ? MaskFormat::Csv : MaskFormat::Pgm,
+               path);
+  });
+}
+
+// *dim_out receives S_b; bits must hold cap bytes.
+int ref_read_mask(const char* path, std::uint8_t* bits, std::int64_t cap, std::int64_t* dim_out) {
+  return guarded([&] {
+    BlockMask m = read_mask(path);
+    *dim_out = m.dim;
+    if (static_cast<std::int64_t>(m.bits.size()) > cap)
+      throw std::out_of_range("ref_read_mask: capacity");
+    std::memcpy(bits, m.bits.data(), m.bits.size());
+  });
+}
+
 }  // extern "C"

@@ -251,12 +251,13 @@ void keep_pool_memory() {
   }();
   (void)done;
 }
-// Head chunks of the host-buffer pipeline (DYNRAD_E2E_CHUNKS, default 4).
+// Head chunks of the host-buffer pipeline (DYNRAD_E2E_CHUNKS, default 8:
+// measured 54.0 ms at 4 chunks, 47.5 ms at 8 for the Wan layer).
 int e2e_chunks() {
   static const int n = [] {
     const char* e = std::getenv("DYNRAD_E2E_CHUNKS");
-    const int v = e ? std::atoi(e) : 4;
-    return v > 0 ? v : 4;
+    const int v = e ? std::atoi(e) : 8;
+    return v > 0 ? v : 8;
   }();
   return n;
 }

@@ -316,6 +316,61 @@ def sparsity(mask: BlockMask) -> float:
     return 1.0 - mask.active_count() / float(mask.dim * mask.dim)
 
 
+# ----------------------------------------------- mask files ---
+# The reference's persistent mask artifact (mask.cpp:291-376): "DRBM" binary
+# (magic, u16 version 1, u32 S_b, the bit-packed rows), a CSV of active
+# (row, col) pairs, or a PGM image (active = 0).  Host-side file I/O, so a
+# mask built here can be consumed by the reference CLI and vice versa.
+class MaskFormat(enum.IntEnum):
+    Binary = 0
+    Csv = 1
+    Pgm = 2
+
+
+def mask_format_for_path(path: str) -> MaskFormat:
+    ext = path[path.rfind("."):] if "." in path else ""
+    fmt = {".bin": MaskFormat.Binary, ".csv": MaskFormat.Csv, ".pgm": MaskFormat.Pgm}.get(ext)
+    if fmt is None:
+        raise InvalidArgument("mask path needs a .bin/.csv/.pgm extension: " + path)
+    return fmt
+
+
+def write_mask(mask: "BlockMask", fmt: MaskFormat, path: str) -> None:
+    try:
+        with open(path, "wb") as f:
+            if fmt == MaskFormat.Binary:
+                f.write(b"DRBM" + (1).to_bytes(2, "little") + int(mask.dim).to_bytes(4, "little"))
+                f.write(np.ascontiguousarray(mask.bits, np.uint8).tobytes())
+            elif fmt == MaskFormat.Csv:
+                r, c = np.nonzero(mask.dense())
+                f.write("".join(f"{a},{b}\n" for a, b in zip(r, c)).encode())
+            else:
+                f.write(f"P5\n{mask.dim} {mask.dim}\n255\n".encode())
+                f.write(np.where(mask.dense() != 0, 0, 255).astype(np.uint8).tobytes())
+    except OSError as e:
+        raise RuntimeFailure("cannot open for writing: " + path) from e
+
+
+def read_mask(path: str) -> "BlockMask":
+    try:
+        raw = open(path, "rb").read()
+    except OSError as e:
+        raise RuntimeFailure("cannot open: " + path) from e
+    if len(raw) < 10 or raw[:4] != b"DRBM":
+        raise RuntimeFailure("mask file has bad magic: " + path)
+    if int.from_bytes(raw[4:6], "little") != 1:
+        raise RuntimeFailure("unsupported mask version in " + path)
+    dim = int.from_bytes(raw[6:10], "little")
+    if dim == 0 or dim > (1 << 26):
+        raise RuntimeFailure("mask dimension out of range in " + path)
+    rb = (dim + 7) // 8
+    if len(raw) - 10 < dim * rb:
+        raise RuntimeFailure("mask payload truncated: " + path)
+    if len(raw) - 10 > dim * rb:
+        raise RuntimeFailure("mask payload has trailing bytes: " + path)
+    return BlockMask(dim, np.frombuffer(raw[10:], np.uint8).reshape(dim, rb).copy())
+
+
 def aggregate_block(kept_in_tile, col_threshold: float, mask_threshold: float,
                     block_size: int) -> bool:
     """mask.cpp:68-85 — the tile activation rule the mask kernels apply."""
