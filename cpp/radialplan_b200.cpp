@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <fstream>
 #include <memory>
 
 #include "plan.hpp"
@@ -422,6 +423,69 @@ bool aggregate_block(const std::vector<std::pair<int, int>>& kept_in_tile, doubl
   int active = 0;
   for (int x : per_col) active += static_cast<double>(x) / block_size >= col_threshold;
   return static_cast<double>(active) / block_size >= mask_threshold;
+}
+
+MaskFormat mask_format_for_path(const std::string& path) {
+  const std::size_t dot = path.rfind('.');
+  const std::string ext = dot == std::string::npos ? std::string() : path.substr(dot);
+  if (ext == ".bin") return MaskFormat::Binary;
+  if (ext == ".csv") return MaskFormat::Csv;
+  if (ext == ".pgm") return MaskFormat::Pgm;
+  throw std::invalid_argument("mask path needs a .bin/.csv/.pgm extension: " + path);
+}
+
+void write_mask(const BlockMask& mask, MaskFormat format, const std::string& path) {
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  if (!f) throw std::runtime_error("cannot open for writing: " + path);
+  if (format == MaskFormat::Binary) {
+    const std::uint32_t dim = static_cast<std::uint32_t>(mask.dim);
+    const unsigned char head[10] = {'D', 'R', 'B', 'M', 1, 0,
+                                    static_cast<unsigned char>(dim),
+                                    static_cast<unsigned char>(dim >> 8),
+                                    static_cast<unsigned char>(dim >> 16),
+                                    static_cast<unsigned char>(dim >> 24)};
+    f.write(reinterpret_cast<const char*>(head), sizeof(head));
+    f.write(reinterpret_cast<const char*>(mask.bits.data()),
+            static_cast<std::streamsize>(mask.bits.size()));
+  } else if (format == MaskFormat::Csv) {
+    std::string text;
+    for (std::int64_t r = 0; r < mask.dim; ++r)
+      for (std::int64_t c = 0; c < mask.dim; ++c)
+        if (mask.get(r, c)) text += std::to_string(r) + "," + std::to_string(c) + "\n";
+    f.write(text.data(), static_cast<std::streamsize>(text.size()));
+  } else {
+    const std::string head = "P5\n" + std::to_string(mask.dim) + " " + std::to_string(mask.dim) +
+                             "\n255\n";
+    f.write(head.data(), static_cast<std::streamsize>(head.size()));
+    std::vector<char> px(static_cast<std::size_t>(mask.dim));
+    for (std::int64_t r = 0; r < mask.dim; ++r) {
+      for (std::int64_t c = 0; c < mask.dim; ++c)
+        px[static_cast<std::size_t>(c)] = mask.get(r, c) ? 0 : static_cast<char>(255);
+      f.write(px.data(), static_cast<std::streamsize>(px.size()));
+    }
+  }
+  if (!f) throw std::runtime_error("write failed: " + path);
+}
+
+BlockMask read_mask(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot open: " + path);
+  unsigned char head[10] = {};
+  f.read(reinterpret_cast<char*>(head), sizeof(head));
+  if (!f || std::memcmp(head, "DRBM", 4) != 0)
+    throw std::runtime_error("mask file has bad magic: " + path);
+  if ((head[4] | (head[5] << 8)) != 1)
+    throw std::runtime_error("unsupported mask version in " + path);
+  const std::uint32_t dim = head[6] | (head[7] << 8) | (static_cast<std::uint32_t>(head[8]) << 16) |
+                            (static_cast<std::uint32_t>(head[9]) << 24);
+  if (dim == 0 || dim > (1u << 26)) throw std::runtime_error("mask dimension out of range in " + path);
+  BlockMask mask(static_cast<std::int64_t>(dim));
+  f.read(reinterpret_cast<char*>(mask.bits.data()), static_cast<std::streamsize>(mask.bits.size()));
+  if (f.gcount() != static_cast<std::streamsize>(mask.bits.size()))
+    throw std::runtime_error("mask payload truncated: " + path);
+  if (f.peek() != std::char_traits<char>::eof())
+    throw std::runtime_error("mask payload has trailing bytes: " + path);
+  return mask;
 }
 
 BlockMask build_mask(const GridSpec& g, const SparsityConfig& c, std::uint64_t seed,

@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 
 #include "radialplan/attention.hpp"
 #include "radialplan/mask.hpp"
@@ -84,6 +86,22 @@ TEST_CASE("aggregate_block (SPEC.md:319)") {
   CHECK(aggregate_block(kept, 0.5, 0.5, 4));
   CHECK_FALSE(aggregate_block(kept, 0.5, 0.6, 4));
   CHECK_THROWS_AS(aggregate_block({{4, 0}}, 0.5, 0.5, 4), std::out_of_range);
+}
+
+TEST_CASE("mask files (mask.cpp:291-376 formats)") {
+  BlockMask m(11);
+  m.set(0, 0);
+  m.set(3, 10);
+  m.set(10, 4);
+  const std::string base = "/tmp/facade_selftest_mask";
+  write_mask(m, mask_format_for_path(base + ".bin"), base + ".bin");
+  CHECK(read_mask(base + ".bin") == m);
+  write_mask(m, MaskFormat::Csv, base + ".csv");
+  std::ifstream csv(base + ".csv");
+  std::string all((std::istreambuf_iterator<char>(csv)), std::istreambuf_iterator<char>());
+  CHECK(all == "0,0\n3,10\n10,4\n");
+  CHECK_THROWS_AS(mask_format_for_path("m.txt"), std::invalid_argument);
+  CHECK_THROWS_AS(read_mask(base + ".csv"), std::runtime_error);
 }
 
 TEST_CASE("GPU operators or a loud failure") {

@@ -256,6 +256,13 @@ struct BuildOptions {
   const FeatureBatch* features = nullptr;  // dynamic mode
 };
 
+// Mask files (mask.hpp:93-101): DRBM binary, CSV of active (row, col), PGM
+// image -- host-side file I/O, byte-compatible with the reference's.
+enum class MaskFormat { Binary, Csv, Pgm };
+MaskFormat mask_format_for_path(const std::string& path);
+void write_mask(const BlockMask& mask, MaskFormat format, const std::string& path);
+BlockMask read_mask(const std::string& path);
+
 // Algorithm 1 on the GPU (stages a-c), returned as a host mask.
 BlockMask build_mask(const GridSpec& g, const SparsityConfig& c, std::uint64_t seed,
                      const BuildOptions& opt = {});
