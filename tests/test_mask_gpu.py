@@ -184,3 +184,21 @@ def test_wan_dynamic_fast_engine_equals_exact_engine(cuda):
     assert st_fast["scored_pairs"] == st_exact["scored_pairs"] == 1599385652
     assert torch.equal(fast, exact)
     assert st_fast["rechecked_pairs"] > 0
+
+
+@pytest.mark.slow
+def test_hunyuan_dynamic_fast_engine_equals_exact_engine(cuda):
+    """BASELINE config 4 at full scale (HunyuanVideo 61x3600, B=128, Table-3
+    Mid, 7.86 G scored pairs): tensor-core engine == exact fp64 engine (the
+    reference's arithmetic)."""
+    g = rp.make_grid(61, 3600, 128)
+    cfg = rp.SparsityConfig(rp.Mode.DynamicThreshold, rp.RadialParams(1.4, 0.7), 0.7, 0.45,
+                            -1.5, 2.0)
+    gen = torch.Generator(device="cuda").manual_seed(43)
+    q = torch.randn((g.total_tokens, 2, 128), device="cuda", generator=gen).to(torch.bfloat16)
+    k = torch.randn((g.total_tokens, 2, 128), device="cuda", generator=gen).to(torch.bfloat16)
+    st = {}
+    fast = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=1)).build_mask_device(q, k, 2, stats=st)
+    exact = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=2)).build_mask_device(q, k, 2)
+    assert st["scored_pairs"] == 7864099452
+    assert torch.equal(fast, exact)
