@@ -535,8 +535,11 @@ BlockMask build_mask(const GridSpec& g, const SparsityConfig& c, std::uint64_t s
 }
 
 // ------------------------------------------------------------- attention --
-std::vector<Eigen::MatrixXf> masked_attention_exact(const FeatureBatch& batch,
-                                                    const TokenMask& mask) {
+namespace {
+// Shared body of masked_attention(_exact): block structure recovered on the
+// device, then the host-buffer C entry point (exact, or soft with eps).
+std::vector<Eigen::MatrixXf> attention_on_gpu(const FeatureBatch& batch, const TokenMask& mask,
+                                              bool soft, double eps) {
   batch.validate(true);
   if (mask.dim < batch.tokens)
     throw std::invalid_argument("masked attention: mask smaller than batch");
@@ -569,8 +572,12 @@ std::vector<Eigen::MatrixXf> masked_attention_exact(const FeatureBatch& batch,
   const std::vector<float> k = pack_heads(batch.keys, n, H, d);
   const std::vector<float> v = pack_heads(batch.values, n, H, d);
   std::vector<float> o(static_cast<std::size_t>(n) * H * d);
-  check(rp_masked_attention_exact_host(&gc, blocks.data(), q.data(), k.data(), v.data(), RP_F32,
-                                       n, H, d, o.data(), nullptr));
+  if (soft)
+    check(rp_masked_attention_host(&gc, blocks.data(), q.data(), k.data(), v.data(), RP_F32, n, H,
+                                   d, eps, o.data(), nullptr));
+  else
+    check(rp_masked_attention_exact_host(&gc, blocks.data(), q.data(), k.data(), v.data(),
+                                         RP_F32, n, H, d, o.data(), nullptr));
   std::vector<Eigen::MatrixXf> out;
   out.reserve(static_cast<std::size_t>(H));
   for (int h = 0; h < H; ++h) {
@@ -580,6 +587,19 @@ std::vector<Eigen::MatrixXf> masked_attention_exact(const FeatureBatch& batch,
     out.push_back(std::move(m));
   }
   return out;
+}
+}  // namespace
+
+std::vector<Eigen::MatrixXf> masked_attention_exact(const FeatureBatch& batch,
+                                                    const TokenMask& mask) {
+  return attention_on_gpu(batch, mask, false, 0.0);
+}
+
+std::vector<Eigen::MatrixXf> masked_attention(const FeatureBatch& batch, const TokenMask& mask,
+                                              double epsilon) {
+  if (!(epsilon > 0.0))
+    throw std::invalid_argument("masked attention: epsilon must be positive");
+  return attention_on_gpu(batch, mask, true, epsilon);
 }
 
 // ----------------------------------------------------- B200 device API ----

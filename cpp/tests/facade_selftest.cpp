@@ -12,6 +12,8 @@
 
 #include <cuda_runtime_api.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -108,6 +110,8 @@ TEST_CASE("GPU operators or a loud failure") {
   const GridSpec g = make_grid(4, 64, 16);
   SparsityConfig c;
   c.near_param = c.far_param = 0.3;
+  CHECK_THROWS_AS(masked_attention(random_batch(64, 1, 8, 5, true), TokenMask(64), 0.0),
+                  std::invalid_argument);  // attention.cpp:109-110, before any device work
   if (!have_gpu()) {
     CHECK_THROWS_AS(build_mask(g, c, 7), std::runtime_error);
     CHECK_THROWS_AS(sparsity(BlockMask(4)), std::runtime_error);
@@ -143,6 +147,12 @@ TEST_CASE("GPU operators or a loud failure") {
   const auto o = masked_attention_exact(b, expand_mask(diag, g3));
   CHECK(o.size() == 1u);
   CHECK(o[0].rows() == 64);
+  // soft mask: at eps -> 0 it approaches the exact variant
+  const auto os = masked_attention(b, expand_mask(diag, g3), 1e-12);
+  float worst = 0.f;
+  for (Eigen::Index r = 0; r < 64; ++r)
+    for (Eigen::Index e = 0; e < 8; ++e) worst = std::max(worst, std::abs(os[0](r, e) - o[0](r, e)));
+  CHECK(worst < 1e-5f);
 }
 
 static int print_mask(int argc, char** argv) {

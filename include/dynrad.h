@@ -288,6 +288,31 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g,
                                          int head_dim, void* o_host,
                                          rp_stream stream);
 
+/* ---------------------------------------------------- soft-mask attention --
+ * masked_attention (attention.hpp:32-39, attention.cpp:59-81, 107-113): every
+ * key takes part; logits get + log1p(epsilon) on active blocks and
+ * + log(epsilon) on inactive ones, then row softmax and the value product.
+ * epsilon must be > 0 (RP_INVALID_ARGUMENT "masked attention: epsilon must be
+ * positive").  Same tensors, dtypes and kernels as rp_sparse_attention_fwd
+ * (bf16: the tcgen05 kernel over dense row lists with a per-block logit
+ * offset; f32: fp64 softmax, 1e-5 parity); mask_bits_dev is the bit-packed
+ * block mask on the device. */
+rp_status rp_soft_attention_fwd(const rp_grid* g, const rp_tensor* q,
+                                const rp_tensor* k, const rp_tensor* v,
+                                rp_tensor* o, const uint8_t* mask_bits_dev,
+                                double epsilon, float softmax_scale,
+                                rp_stream stream);
+
+/* Host-buffer soft-mask attention (the reference's masked_attention calling
+ * convention; buffers as in rp_masked_attention_exact_host). */
+rp_status rp_masked_attention_host(const rp_grid* g,
+                                   const uint8_t* mask_bits_host,
+                                   const void* q_host, const void* k_host,
+                                   const void* v_host, int dtype,
+                                   int64_t tokens, int heads, int head_dim,
+                                   double epsilon, void* o_host,
+                                   rp_stream stream);
+
 /* Number of CUDA kernels this library has launched in the calling process
  * (all entry points); used by bench.py to report gpu_launches. */
 int64_t rp_kernel_launch_count(void);

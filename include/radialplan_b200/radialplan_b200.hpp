@@ -276,6 +276,13 @@ BlockMask build_mask(const GridSpec& g, const SparsityConfig& c, std::uint64_t s
 std::vector<Eigen::MatrixXf> masked_attention_exact(const FeatureBatch& batch,
                                                     const TokenMask& mask);
 
+// masked_attention (attention.hpp:32-39, attention.cpp:59-81, 107-113): soft
+// mask, logits + log(mask + epsilon) (log1p(eps) on active blocks, log(eps)
+// elsewhere), on the GPU with the same precision as masked_attention_exact.
+// Throws std::invalid_argument unless epsilon > 0.
+std::vector<Eigen::MatrixXf> masked_attention(const FeatureBatch& batch, const TokenMask& mask,
+                                              double epsilon = 1e-10);
+
 // ======================================= B200 device API (beyond the ref) ==
 namespace b200 {
 

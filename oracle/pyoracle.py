@@ -278,6 +278,9 @@ class _PortLib(_Lib):
         L.orc_masked_attention_exact.argtypes = [_P(_Grid), _u8p, _f32p, _f32p, _f32p,
                                                  C.c_int64, C.c_int, C.c_int, C.c_int64,
                                                  C.c_int64, _f32p, C.c_int]
+        L.orc_masked_attention.argtypes = [_P(_Grid), _u8p, _f32p, _f32p, _f32p, C.c_int64,
+                                           C.c_int, C.c_int, C.c_double, C.c_int64,
+                                           C.c_int64, _f32p, C.c_int]
         L.orc_random_batch.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, _f32p, _f32p,
                                        _f32p, C.c_int]
         L.orc_mix64.argtypes = [C.c_uint64]
@@ -316,7 +319,8 @@ class _PortLib(_Lib):
         return out
 
     def masked_attention_exact(self, nf, nt, bs, bits, q, k, v, row_begin=0, row_end=None,
-                               threads=1):
+                               threads=1, eps=None):
+        """eps None: masked_attention_exact; eps > 0: soft-mask masked_attention."""
         g = self._grid(nf, nt, bs)
         if row_end is None:
             row_end = g.padded_tokens
@@ -326,10 +330,19 @@ class _PortLib(_Lib):
         tok, h, d = q.shape
         out = np.zeros((row_end - row_begin, h, d), np.float32)
         bits = np.ascontiguousarray(bits, np.uint8)
-        self._chk(self.lib.orc_masked_attention_exact(C.byref(g), bits.ctypes.data_as(_u8p),
-                                                      _fp(q), _fp(k), _fp(v), tok, h, d,
-                                                      row_begin, row_end, _fp(out), threads))
+        if eps is None:
+            rc = self.lib.orc_masked_attention_exact(C.byref(g), bits.ctypes.data_as(_u8p),
+                                                     _fp(q), _fp(k), _fp(v), tok, h, d,
+                                                     row_begin, row_end, _fp(out), threads)
+        else:
+            rc = self.lib.orc_masked_attention(C.byref(g), bits.ctypes.data_as(_u8p), _fp(q),
+                                               _fp(k), _fp(v), tok, h, d, float(eps),
+                                               row_begin, row_end, _fp(out), threads)
+        self._chk(rc)
         return out
+
+    def masked_attention(self, nf, nt, bs, bits, q, k, v, eps=1e-10, **kw):
+        return self.masked_attention_exact(nf, nt, bs, bits, q, k, v, eps=eps, **kw)
 
     def random_batch(self, tokens, heads, d, seed, with_values=True, threads=1):
         q = np.zeros((tokens, heads, d), np.float32)

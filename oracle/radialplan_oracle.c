@@ -467,6 +467,8 @@ typedef struct {
   int64_t rb, re, row0;
   float* out;
   int status;
+  int soft;            /* masked_attention (attention.cpp:59-81): log1p/log eps offsets */
+  double log_active, log_inactive;
 } attn_t;
 
 static void* attn_run(void* arg) {
@@ -483,7 +485,8 @@ static void* attn_run(void* arg) {
       double m = -INFINITY;
       for (int64_t c = 0; c < n; ++c) {
         const int64_t bc = c / bs;
-        if (!((a->bits[br * row_bytes + bc / 8] >> (bc % 8)) & 1u)) {
+        const int active = (a->bits[br * row_bytes + bc / 8] >> (bc % 8)) & 1u;
+        if (!a->soft && !active) {
           p[c] = -INFINITY;
           continue;
         }
@@ -494,7 +497,8 @@ static void* attn_run(void* arg) {
           const float* kb = a->k + (c * heads + h) * d;
           for (int e = 0; e < d; ++e) logit += qa[e] * kb[e];
         }
-        const double l = (double)logit * scale;
+        const double l = (double)logit * scale +
+                         (a->soft ? (active ? a->log_active : a->log_inactive) : 0.0);
         p[c] = l;
         if (l > m) m = l;
       }
@@ -519,11 +523,9 @@ done:
   return NULL;
 }
 
-int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
-                               const float* q, const float* k, const float* v,
-                               int64_t tokens, int heads, int d,
-                               int64_t row_begin, int64_t row_end, float* out,
-                               int threads) {
+static int attention(const orc_grid* g, const uint8_t* bits, const float* q, const float* k,
+                     const float* v, int64_t tokens, int heads, int d, int soft, double eps,
+                     int64_t row_begin, int64_t row_end, float* out, int threads) {
   if (tokens < 1 || heads < 1 || d < 1) {
     snprintf(g_err, sizeof g_err, "feature batch: empty dimensions");
     return 1;
@@ -542,6 +544,9 @@ int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
     attn_t* a = &as[w];
     a->g = g; a->bits = bits; a->q = q; a->k = k; a->v = v; a->tokens = tokens;
     a->heads = heads; a->d = d; a->row0 = row_begin; a->out = out;
+    a->soft = soft;
+    a->log_active = soft ? log1p(eps) : 0.0;
+    a->log_inactive = soft ? log(eps) : 0.0;
     a->rb = row_begin + w * chunk;
     a->re = row_begin + (w + 1) * chunk < row_end ? row_begin + (w + 1) * chunk : row_end;
     if (a->rb > a->re) a->rb = a->re;
@@ -557,6 +562,28 @@ int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
   free(as);
   if (st == 3) snprintf(g_err, sizeof g_err, "masked attention: row has no active key");
   return st;
+}
+
+int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
+                               const float* q, const float* k, const float* v,
+                               int64_t tokens, int heads, int d,
+                               int64_t row_begin, int64_t row_end, float* out,
+                               int threads) {
+  return attention(g, bits, q, k, v, tokens, heads, d, 0, 0.0, row_begin, row_end, out,
+                   threads);
+}
+
+/* masked_attention (attention.cpp:107-113): epsilon must be positive. */
+int orc_masked_attention(const orc_grid* g, const uint8_t* bits, const float* q,
+                         const float* k, const float* v, int64_t tokens, int heads, int d,
+                         double eps, int64_t row_begin, int64_t row_end, float* out,
+                         int threads) {
+  if (!(eps > 0.0)) {
+    snprintf(g_err, sizeof g_err, "masked attention: epsilon must be positive");
+    return 1;
+  }
+  return attention(g, bits, q, k, v, tokens, heads, d, 1, eps, row_begin, row_end, out,
+                   threads);
 }
 
 /* ---- random_batch (attention.cpp:182-204; rng.hpp:84-91) --------------- */

@@ -151,6 +151,10 @@ _SIGS = {
                                  _v, _v, C.c_float, _v], C.c_int),
     "rp_masked_attention_exact_host": ([_P(Grid), _v, _v, _v, _v, C.c_int, C.c_int64, C.c_int,
                                         C.c_int, _v, _v], C.c_int),
+    "rp_soft_attention_fwd": ([_P(Grid), _P(Tensor), _P(Tensor), _P(Tensor), _P(Tensor), _v,
+                               C.c_double, C.c_float, _v], C.c_int),
+    "rp_masked_attention_host": ([_P(Grid), _v, _v, _v, _v, C.c_int, C.c_int64, C.c_int,
+                                  C.c_int, C.c_double, _v, _v], C.c_int),
     "rp_static_select": ([_P(Band), C.c_double, C.c_uint64, _v, C.c_int64, _P(C.c_int64), _v],
                          C.c_int),
     "rp_proxy_scores": ([_P(Tensor), _P(Tensor), C.c_int, _P(Band), _v, _v], C.c_int),

@@ -31,6 +31,11 @@ struct Params {
   const int32_t* col_idx;
   double scale;
   int* error_flag;   // set to 1 on an empty row (domain_error)
+  // Soft mask (masked_attention, attention.cpp:59-81; null = exact): dense
+  // row lists, logit + log1p(eps) on active blocks, + log(eps) elsewhere.
+  const uint8_t* soft_bits;
+  long long soft_row_bytes;
+  double log_active, log_inactive;
 };
 
 __global__ void __launch_bounds__(kThreads)
@@ -74,7 +79,12 @@ __global__ void __launch_bounds__(kThreads)
       const int beg = p.row_ptr[br], end = p.row_ptr[br + 1];
       const bool mine = row_ok && br == brow;
       for (int bi = beg; bi < end; ++bi) {
-        const long long c0 = static_cast<long long>(p.col_idx[bi]) * p.block;
+        const int cb = p.col_idx[bi];
+        const long long c0 = static_cast<long long>(cb) * p.block;
+        double off = 0.0;
+        if (p.soft_bits && mine)
+          off = ((p.soft_bits[brow * p.soft_row_bytes + (cb >> 3)] >> (cb & 7)) & 1) ? p.log_active
+                                                                                  : p.log_inactive;
         for (int k0 = 0; k0 < p.block; k0 += kKeys) {
           const int nk = min(kKeys, p.block - k0);
           __syncthreads();
@@ -90,7 +100,7 @@ __global__ void __launch_bounds__(kThreads)
           for (int kk = sub; kk < nk; kk += 4) {
             float lg = 0.f;
             for (int e = 0; e < d; ++e) lg = fmaf(sq[r][e], sk[kk][e], lg);
-            const double l = static_cast<double>(lg) * p.scale;
+            const double l = static_cast<double>(lg) * p.scale + off;
             if (pass == 0) {
               if (mine && l > m) m = l;
             } else {

@@ -76,6 +76,13 @@ struct Params {
   long long out_tok_stride;
   long long out_head_stride;
   float scale_log2;
+  // Soft mask (masked_attention, attention.cpp:59-81; null = exact mask):
+  // the row lists are dense and a block whose bit is clear gets the logit
+  // offset soft_delta = (log eps - log1p eps) / scale (raw-logit units; the
+  // common log1p eps of active blocks cancels in the softmax).
+  const uint8_t* soft_bits;
+  long long soft_row_bytes;
+  float soft_delta;
 };
 
 #ifdef RP_TRACE
@@ -374,6 +381,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < n; ++j, ++g) {
         const uint32_t b = g & 1;
         const uint32_t sb = b * 128;
+        float dlt = 0.f;  // soft-mask offset of this block (0: exact mode / active)
+        if (p.soft_bits) {
+          const int c = __ldg(p.col_idx + beg + j);
+          const uint8_t by = __ldg(p.soft_bits + row * p.soft_row_bytes + (c >> 3));
+          dlt = ((by >> (c & 7)) & 1) ? 0.f : p.soft_delta;
+        }
         if (tr) RP_TR2(0, g);
         mbar_wait(&s_full[b], (g >> 1) & 1);
         if (tr) RP_TR2(1, g);
@@ -397,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float a = S(0);
 #pragma unroll
           for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
-          m = exchange_max(fmaxf(a, S(63)));
+          m = exchange_max(fmaxf(a, S(63)) + dlt);
         }
         // p = 2^((s - m) * scale * log2 e) against the running reference m
         // (stale: the max of the previous blocks, so the exponentials do not
@@ -409,7 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float lmax = -INFINITY;
         auto exps = [&](float mref, bool track) {
           const float2 sc2 = make_float2(sl2, sl2);
-          const float2 ng2 = make_float2(-mref * sl2, -mref * sl2);
+          const float nb = (dlt - mref) * sl2;
+          const float2 ng2 = make_float2(nb, nb);
           acc[0] = acc[1] = make_float2(0.f, 0.f);
           float2 pv_prev[16];
 #pragma unroll
@@ -442,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // this block's max (both halves): if it overtook the reference by
           // more than 2^8, rebase O and l on the new max and redo the block
           // (rare after the first blocks; exact either way)
-          const float mx = exchange_max(lmax);
+          const float mx = exchange_max(lmax + dlt);
           const bool need = (mx - m) * sl2 > 8.0f;
           if (__any_sync(0xFFFFFFFFu, need)) {
             const float alpha = need ? ex2((m - mx) * sl2) : 1.0f;

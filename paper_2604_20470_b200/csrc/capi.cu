@@ -54,7 +54,10 @@ static void check_tensor(const rp_tensor* t, const char* name) {
 static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tensor& k,
                              const rp_tensor& v, rp_tensor& o, const int32_t* row_ptr,
                              const int32_t* col_idx, const int32_t* row_order, float scale,
-                             cudaStream_t stream, int* err_flag) {
+                             cudaStream_t stream, int* err_flag,
+                             const uint8_t* soft_bits = nullptr, double eps = 0.0) {
+  // soft_bits != null: soft mask (masked_attention, attention.cpp:59-81) over
+  // dense row lists; the block bit selects the log1p(eps) / log(eps) offset
   const int d = q.head_dim;
   const float user_scale = scale;
   if (scale <= 0.f) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
@@ -91,7 +94,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       done = true;
     };
-    if (variant == 0) {
+    if (variant == 0 && !soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
@@ -159,6 +162,11 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.out_tok_stride = o.token_stride;
       p.out_head_stride = o.head_stride;
       p.scale_log2 = scale * 1.4426950408889634f;
+      p.soft_bits = soft_bits;
+      p.soft_row_bytes = g.row_bytes;
+      p.soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
+                                                    static_cast<double>(scale))
+                               : 0.f;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
       if (d == 128) {
         static bool done = false;
@@ -196,6 +204,10 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     p.scale = user_scale > 0.f ? static_cast<double>(user_scale)
                                : 1.0 / std::sqrt(static_cast<double>(d));
     p.error_flag = err_flag;
+    p.soft_bits = soft_bits;
+    p.soft_row_bytes = g.row_bytes;
+    p.log_active = soft_bits ? std::log1p(eps) : 0.0;
+    p.log_inactive = soft_bits ? std::log(eps) : 0.0;
     dim3 grid(static_cast<unsigned>((g.padded_tokens + attn32::kRows - 1) / attn32::kRows),
               static_cast<unsigned>(q.heads));
     attn32::attn_f32_kernel<<<grid, attn32::kThreads, 0, stream>>>(p);
@@ -408,12 +420,14 @@ rp_status rp_mask_sparsity(const rp_grid* g, const uint8_t* bits, int64_t* activ
   });
 }
 
-rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_bits_host,
-                                         const void* q_host, const void* k_host,
-                                         const void* v_host, int dtype, int64_t tokens,
-                                         int heads, int head_dim, void* o_host,
-                                         rp_stream stream) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace rp {
+// Host-buffer attention (exact: soft == false; soft mask with eps otherwise).
+static void host_attention(const rp_grid* g, const uint8_t* mask_bits_host, const void* q_host,
+                           const void* k_host, const void* v_host, int dtype, int64_t tokens,
+                           int heads, int head_dim, void* o_host, rp_stream stream, bool soft,
+                           double eps) {
     require_device();
     check_grid(g);
     if (tokens < 1 || heads < 1 || head_dim < 1)
@@ -449,17 +463,24 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_b
     alloc(&ro, sizeof(int32_t) * nb);
     alloc(&cnt, sizeof(int32_t) * (nb + 1));
     alloc(&flag, sizeof(int));
-    // Row lists first: an empty row is a domain_error in the reference
-    // (attention.cpp:85-86), detected before any feature is moved.
     RP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
     RP_CUDA(cudaMemcpyAsync(dm, mask_bits_host, mask_bytes, cudaMemcpyHostToDevice, s));
-    launch_csr(*g, dm, rp_, ci, nb * nb, ro, nullptr, cnt, s);
-    std::vector<int32_t> hcnt(static_cast<size_t>(nb) + 1);
-    RP_CUDA(cudaMemcpyAsync(hcnt.data(), rp_, sizeof(int32_t) * (nb + 1),
-                            cudaMemcpyDeviceToHost, s));
-    RP_CUDA(cudaStreamSynchronize(s));
-    for (int64_t r = 0; r < nb; ++r)
-      if (hcnt[r + 1] == hcnt[r]) throw std::domain_error("masked attention: row has no active key");
+    if (soft) {
+      csr::dense_lists_kernel<<<static_cast<unsigned>((nb * nb + 255) / 256), 256, 0, s>>>(nb, rp_, ci);
+      RP_LAUNCHED();
+      ro = nullptr;
+    } else {
+      // Row lists first: an empty row is a domain_error in the reference
+      // (attention.cpp:85-86), detected before any feature is moved.
+      launch_csr(*g, dm, rp_, ci, nb * nb, ro, nullptr, cnt, s);
+      std::vector<int32_t> hcnt(static_cast<size_t>(nb) + 1);
+      RP_CUDA(cudaMemcpyAsync(hcnt.data(), rp_, sizeof(int32_t) * (nb + 1),
+                              cudaMemcpyDeviceToHost, s));
+      RP_CUDA(cudaStreamSynchronize(s));
+      for (int64_t r = 0; r < nb; ++r)
+        if (hcnt[r + 1] == hcnt[r])
+          throw std::domain_error("masked attention: row has no active key");
+    }
     alloc(&dq, in_bytes);
     alloc(&dk, in_bytes);
     alloc(&dv, in_bytes);
@@ -500,7 +521,7 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_b
       rp_tensor to = tq;
       to.data = dout + off;
       to.tokens = g->padded_tokens;
-      launch_attention(*g, tq, tk, tv, to, rp_, ci, ro, 0.f, s, flag);
+      launch_attention(*g, tq, tk, tv, to, rp_, ci, ro, 0.f, s, flag, soft ? dm : nullptr, eps);
       cudaEvent_t k_done = event();
       RP_CUDA(cudaEventRecord(k_done, s));
       RP_CUDA(cudaStreamWaitEvent(hs.out, k_done, 0));
@@ -514,6 +535,68 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_b
     RP_CUDA(cudaStreamSynchronize(s));
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     cudaEventDestroy(start_ev);
+}
+
+static void check_epsilon(double eps) {
+  if (!(eps > 0.0)) throw std::invalid_argument("masked attention: epsilon must be positive");
+}
+}  // namespace rp
+
+extern "C" {
+
+rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_bits_host,
+                                         const void* q_host, const void* k_host,
+                                         const void* v_host, int dtype, int64_t tokens,
+                                         int heads, int head_dim, void* o_host,
+                                         rp_stream stream) {
+  return guarded([&] {
+    host_attention(g, mask_bits_host, q_host, k_host, v_host, dtype, tokens, heads, head_dim,
+                   o_host, stream, false, 0.0);
+  });
+}
+
+rp_status rp_masked_attention_host(const rp_grid* g, const uint8_t* mask_bits_host,
+                                   const void* q_host, const void* k_host, const void* v_host,
+                                   int dtype, int64_t tokens, int heads, int head_dim,
+                                   double epsilon, void* o_host, rp_stream stream) {
+  return guarded([&] {
+    check_epsilon(epsilon);
+    host_attention(g, mask_bits_host, q_host, k_host, v_host, dtype, tokens, heads, head_dim,
+                   o_host, stream, true, epsilon);
+  });
+}
+
+rp_status rp_soft_attention_fwd(const rp_grid* g, const rp_tensor* q, const rp_tensor* k,
+                                const rp_tensor* v, rp_tensor* o, const uint8_t* mask_bits_dev,
+                                double epsilon, float softmax_scale, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    check_epsilon(epsilon);
+    check_tensor(q, "q");
+    check_tensor(k, "k");
+    check_tensor(v, "v");
+    check_tensor(o, "o");
+    if (k->tokens != q->tokens || v->tokens != q->tokens || k->heads != q->heads ||
+        v->heads != q->heads || k->head_dim != q->head_dim || v->head_dim != q->head_dim ||
+        k->dtype != q->dtype || v->dtype != q->dtype || o->dtype != q->dtype)
+      throw std::invalid_argument("feature batch: queries/keys/values shape mismatch");
+    if (g->padded_tokens < q->tokens)
+      throw std::invalid_argument("masked attention: mask smaller than batch");
+    if (o->tokens < g->padded_tokens || o->heads != q->heads || o->head_dim != q->head_dim)
+      throw std::invalid_argument("masked attention: output must be [S', heads, head_dim]");
+    if (!mask_bits_dev) throw std::invalid_argument("masked attention: null mask");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nb = g->blocks_per_dim;
+    int32_t *rp_ = nullptr, *ci = nullptr;
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rp_), sizeof(int32_t) * (nb + 1), s));
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ci), sizeof(int32_t) * nb * nb, s));
+    csr::dense_lists_kernel<<<static_cast<unsigned>((nb * nb + 255) / 256), 256, 0, s>>>(nb, rp_, ci);
+    RP_LAUNCHED();
+    launch_attention(*g, *q, *k, *v, *o, rp_, ci, nullptr, softmax_scale, s, nullptr,
+                     mask_bits_dev, epsilon);
+    RP_CUDA(cudaFreeAsync(rp_, s));
+    RP_CUDA(cudaFreeAsync(ci, s));
   });
 }
 

@@ -137,5 +137,14 @@ __global__ void popcount_kernel(const uint8_t* __restrict__ bits, int64_t n,
   if (threadIdx.x % 32 == 0) atomicAdd(out, c);
 }
 
+// Dense row lists (every block of every row) for the soft-mask path:
+// row_ptr[r] = r * n, col_idx[r * n + c] = c.
+__global__ void dense_lists_kernel(int64_t n, int32_t* __restrict__ row_ptr,
+                                   int32_t* __restrict__ col_idx) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i <= n) row_ptr[i] = static_cast<int32_t>(i * n);
+  if (i < n * n) col_idx[i] = static_cast<int32_t>(i % n);
+}
+
 }  // namespace csr
 }  // namespace rp

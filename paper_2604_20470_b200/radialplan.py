@@ -617,13 +617,25 @@ def expand_mask(mask_dev, g: GridSpec, stream=None):
     return out
 
 
-def masked_attention_exact(g: GridSpec, mask: BlockMask, q: np.ndarray, k: np.ndarray,
-                           v: np.ndarray) -> np.ndarray:
-    """masked_attention_exact (attention.hpp:43-44) with host buffers.
+def soft_attention(g: GridSpec, q, k, v, mask_dev, epsilon: float, out=None,
+                   softmax_scale: float = 0.0, stream=None):
+    """Soft-mask attention (masked_attention, attention.cpp:59-81) on device
+    tensors: every key attended, logits + log1p(eps) on active blocks and
+    + log(eps) elsewhere.  mask_dev: the bit-packed block mask on the GPU."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((g.padded_tokens, q.shape[1], q.shape[2]), dtype=q.dtype,
+                          device=q.device)
+    gc = g.c()
+    tq, tk, tv, to = _tensor(q), _tensor(k), _tensor(v), _tensor(out)
+    L.check(L.lib().rp_soft_attention_fwd(
+        C.byref(gc), C.byref(tq), C.byref(tk), C.byref(tv), C.byref(to),
+        C.c_void_p(mask_dev.data_ptr()), C.c_double(epsilon), C.c_float(softmax_scale),
+        _stream(stream)))
+    return out
 
-    q/k/v: host float32 (or bf16 as uint16) arrays [tokens, heads, d];
-    returns host [S', heads, d].  Raises DomainError on an empty row.
-    """
+
+def _host_attention(fn, g: GridSpec, mask: BlockMask, q, k, v, *extra):
     q = np.ascontiguousarray(q)
     k = np.ascontiguousarray(k)
     v = np.ascontiguousarray(v)
@@ -632,16 +644,33 @@ def masked_attention_exact(g: GridSpec, mask: BlockMask, q: np.ndarray, k: np.nd
     elif q.dtype == np.uint16:
         code, odt = L.RP_BF16, np.uint16
     else:
-        raise InvalidArgument("masked_attention_exact: float32 or bf16 (uint16) inputs")
+        raise InvalidArgument("masked attention: float32 or bf16 (uint16) inputs")
     tok, h, d = q.shape
     out = np.empty((g.padded_tokens, h, d), odt)
     bits = np.ascontiguousarray(mask.bits, np.uint8)
     gc = g.c()
-    L.check(L.lib().rp_masked_attention_exact_host(
-        C.byref(gc), bits.ctypes.data_as(C.c_void_p), q.ctypes.data_as(C.c_void_p),
-        k.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p), code, tok, h, d,
-        out.ctypes.data_as(C.c_void_p), None))
+    L.check(fn(C.byref(gc), bits.ctypes.data_as(C.c_void_p), q.ctypes.data_as(C.c_void_p),
+               k.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p), code, tok, h, d,
+               *extra, out.ctypes.data_as(C.c_void_p), None))
     return out
+
+
+def masked_attention_exact(g: GridSpec, mask: BlockMask, q: np.ndarray, k: np.ndarray,
+                           v: np.ndarray) -> np.ndarray:
+    """masked_attention_exact (attention.hpp:43-44) with host buffers.
+
+    q/k/v: host float32 (or bf16 as uint16) arrays [tokens, heads, d];
+    returns host [S', heads, d].  Raises DomainError on an empty row.
+    """
+    return _host_attention(L.lib().rp_masked_attention_exact_host, g, mask, q, k, v)
+
+
+def masked_attention(g: GridSpec, mask: BlockMask, q: np.ndarray, k: np.ndarray,
+                     v: np.ndarray, epsilon: float = 1e-10) -> np.ndarray:
+    """masked_attention (attention.hpp:37-39, soft mask log(mask + eps)) with
+    host buffers; raises InvalidArgument unless epsilon > 0."""
+    return _host_attention(L.lib().rp_masked_attention_host, g, mask, q, k, v,
+                           C.c_double(epsilon))
 
 
 class PooledMode(enum.IntEnum):

@@ -39,19 +39,41 @@ def _(q, k, v, row_ptr, col_idx, row_order, n_frames, tokens_per_frame, block_si
     return q.new_empty((padded, q.shape[1], q.shape[2]))
 
 
+@torch.library.custom_op("dynrad::soft_attention", mutates_args=())
+def soft_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask_bits: torch.Tensor,
+                   epsilon: float, n_frames: int, tokens_per_frame: int, block_size: int,
+                   softmax_scale: float = 0.0) -> torch.Tensor:
+    """Soft-mask attention (masked_attention, attention.cpp:59-81): every key,
+    logits + log1p(eps) on active blocks and + log(eps) elsewhere."""
+    g = rp.make_grid(n_frames, tokens_per_frame, block_size)
+    return rp.soft_attention(g, q, k, v, mask_bits, epsilon, softmax_scale=softmax_scale)
+
+
+@soft_attention.register_fake
+def _(q, k, v, mask_bits, epsilon, n_frames, tokens_per_frame, block_size, softmax_scale=0.0):
+    padded = (n_frames * tokens_per_frame + block_size - 1) // block_size * block_size
+    return q.new_empty((padded, q.shape[1], q.shape[2]))
+
+
 class RadialSparseAttention(torch.nn.Module):
     """Attention core of one DiT layer over an (N_f, h*w) latent grid.
 
     forward(q, k, v) with q/k/v bf16 [tokens, heads, head_dim] returns
     [tokens, heads, head_dim] (the padded rows are dropped).  Static mode
     builds the mask once per (grid, config, seed) and reuses it; dynamic mode
-    rebuilds it every call from the first ``n_score_heads`` heads.
+    rebuilds it every call from the first ``n_score_heads`` heads.  With
+    ``soft_epsilon`` set, the layer runs the reference's default soft-mask
+    semantics (masked_attention) instead of the exact block-sparse kernel.
     """
 
     def __init__(self, n_frames: int, tokens_per_frame: int, config: rp.SparsityConfig,
                  seed: int = 7, block_size: int = 128, n_score_heads: int = 2,
-                 softmax_scale: float = 0.0):
+                 softmax_scale: float = 0.0, soft_epsilon: Optional[float] = None):
         super().__init__()
+        if soft_epsilon is not None and not soft_epsilon > 0:
+            raise rp.InvalidArgument("masked attention: epsilon must be positive")
+        self.soft_epsilon = soft_epsilon
+        self._mask = None
         self.grid = rp.make_grid(n_frames, tokens_per_frame, block_size)
         self.config = config
         self.plan = rp.Plan(self.grid, config, seed)
@@ -71,9 +93,21 @@ class RadialSparseAttention(torch.nn.Module):
             self._lists = rp.mask_to_csr(self.grid, self.plan.build_mask_device())
         return self._lists
 
+    def mask(self, q: Optional[torch.Tensor] = None, k: Optional[torch.Tensor] = None):
+        if self.dynamic:
+            return self.plan.build_mask_device(q, k, self.n_score_heads)
+        if self._mask is None:
+            self._mask = self.plan.build_mask_device()
+        return self._mask
+
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
-        row_ptr, col_idx, order = self.block_lists(q, k)
         g = self.grid
+        if self.soft_epsilon is not None:
+            out = torch.ops.dynrad.soft_attention(q, k, v, self.mask(q, k), self.soft_epsilon,
+                                                  g.n_frames, g.tokens_per_frame, g.block_size,
+                                                  self.softmax_scale)
+            return out[: g.total_tokens]
+        row_ptr, col_idx, order = self.block_lists(q, k)
         out = torch.ops.dynrad.sparse_attention(q, k, v, row_ptr, col_idx, order, g.n_frames,
                                                 g.tokens_per_frame, g.block_size,
                                                 self.softmax_scale)

@@ -8,7 +8,8 @@ oracle/Makefile; needs /root/reference in this container) and writes:
   wan_cfg3.drbm     Wan2.1 21x3600 B=128 static config-3 mask (SURVEY §8d:
                     gamma 1.0, lambda 0.1, theta_m 1.0, theta_c 0.2,
                     rho .3/.3, seed 7), DRBM format (mask.cpp:301-347)
-  attn_small.npz    masked_attention_exact outputs on a small padded grid
+  attn_small.npz    masked_attention_exact and soft-mask masked_attention
+                    (eps 1e-10, 1e-3, 0.25, 4) outputs on a small padded grid
 
 Features for dynamic cases are random_batch(S, H_f=2, d, seed) (the
 reference's counter-based generator, attention.cpp:182-204), which the C
@@ -115,8 +116,13 @@ def main():
     mbits = R.build_mask(nf, nt, bs, Cfg(0, 1.0, 1.0, 1e-6, 0.5, 0.2, 0.5, 0.5), 3)
     exact = R.masked_attention(nf, nt, bs, mbits, q, k, v, exact=True)
     soft = R.masked_attention(nf, nt, bs, mbits, q, k, v, exact=False)
+    # soft mask at epsilons where inactive blocks carry visible mass
+    soft_eps = np.array([1e-3, 0.25, 4.0])
+    soft_multi = np.stack([R.masked_attention(nf, nt, bs, mbits, q, k, v, exact=False, eps=e)
+                           for e in soft_eps])
     np.savez_compressed(os.path.join(HERE, "attn_small.npz"), nf=nf, nt=nt, bs=bs, seed=17,
-                        bits=mbits, exact=exact, soft=soft)
+                        bits=mbits, exact=exact, soft=soft, soft_eps=soft_eps,
+                        soft_multi=soft_multi)
     print(f"{len(cases)} mask cases; wan cfg3 active={int(np.unpackbits(bits).sum())}")
 
 

@@ -120,3 +120,17 @@ def test_reference_library_and_oracle_disagree_on_disable_split(ref):
         assert same_split
         differ += not np.array_equal(np.asarray(lib), np.asarray(orc))
     assert differ == 5
+
+
+def test_soft_attention_restatement_vs_reference_golden(port):
+    """masked_attention (attention.cpp:59-81) soft mask at four epsilons."""
+    z = np.load(f"{GOLDEN}/attn_small.npz")
+    nf, nt, bs = int(z["nf"]), int(z["nt"]), int(z["bs"])
+    q, k, v = port.random_batch(nf * nt, 2, 32, int(z["seed"]), threads=2)
+    out = port.masked_attention(nf, nt, bs, z["bits"], q, k, v, eps=1e-10, threads=4)
+    assert np.abs(out - z["soft"]).max() <= 1e-6
+    for eps, want in zip(z["soft_eps"], z["soft_multi"]):
+        out = port.masked_attention(nf, nt, bs, z["bits"], q, k, v, eps=float(eps), threads=4)
+        assert np.abs(out - want).max() <= 1e-6, eps
+    with pytest.raises(pyoracle.OracleError):
+        port.masked_attention(nf, nt, bs, z["bits"], q, k, v, eps=0.0)
