@@ -313,6 +313,51 @@ rp_status rp_masked_attention_host(const rp_grid* g,
                                    double epsilon, void* o_host,
                                    rp_stream stream);
 
+/* ------------------------------------------- profiler objective --
+ * build_proxy_cache (profiler.hpp:58-66, profiler.cpp:49-78) and objective
+ * (profiler.hpp:68-76, profiler.cpp:80-148) on the GPU.  The cache is
+ * device-resident and opaque: per-(row, column block) sums of the dense
+ * proxy attention numerators w and w^2, the diagonal, the row sums and
+ * |A_dense|_F^2 -- everything a trial reads -- instead of the S x S matrix.
+ * features_dev: the ProxyBatch features, [total_tokens, feature_dim] f32
+ * row-major on the device.  The logits follow the reference's float GEMM
+ * order, exp runs in double (see csrc/objective.cu for the contract). */
+typedef struct rp_proxy_cache rp_proxy_cache;
+
+typedef struct {
+  double loss; /* mse + penalty_weight * max(0, sparsity_target - achieved) */
+  double mse;  /* masked-vs-dense reconstruction error over real tokens */
+  double achieved_sparsity; /* over the padded block grid */
+} rp_trial;
+
+/* Synchronous.  The grid is ProxyBatch::grid. */
+rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev,
+                                int feature_dim, rp_proxy_cache** out,
+                                rp_stream stream);
+
+/* From a reference-layout DenseProxyCache already on the device: weights
+ * [S, S] f32 row-major, row_sums [S] f64, and its reference_sq_norm. */
+rp_status rp_proxy_cache_from_weights(const rp_grid* g, const float* weights_dev,
+                                      const double* row_sums_dev,
+                                      double reference_sq_norm,
+                                      rp_proxy_cache** out, rp_stream stream);
+
+void rp_proxy_cache_destroy(rp_proxy_cache* cache);
+
+/* Copies row_sums [S] (may be NULL) and reference_sq_norm to the host. */
+rp_status rp_proxy_cache_stats(const rp_proxy_cache* cache, double* row_sums_host,
+                               double* reference_sq_norm, rp_stream stream);
+
+/* One trial: validates c, builds the mask with seed mix64(batch_seed,
+ * 0x6d61736b) on the GPU (dynamic mode scores scoring_features(batch), i.e.
+ * the features as one fused head), then the error and loss.  Synchronous.
+ * mask_bits_dev (may be NULL) receives the trial's bit-packed mask. */
+rp_status rp_objective(const rp_proxy_cache* cache, const rp_config* c,
+                       uint64_t batch_seed, const float* features_dev,
+                       int feature_dim, double penalty_weight,
+                       double sparsity_target, rp_trial* out,
+                       uint8_t* mask_bits_dev, rp_stream stream);
+
 /* Number of CUDA kernels this library has launched in the calling process
  * (all entry points); used by bench.py to report gpu_launches. */
 int64_t rp_kernel_launch_count(void);

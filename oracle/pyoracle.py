@@ -156,6 +156,12 @@ class _RefLib(_Lib):
                                        _f32p, _f32p, C.c_int64, C.c_int, C.c_int, _f32p,
                                        _P(C.c_double), _P(C.c_double)]
         L.ref_write_mask.argtypes = [_u8p, C.c_int64, C.c_int, C.c_char_p]
+        L.ref_simulate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
+                                   C.c_uint64, _f32p]
+        L.ref_proxy_cache.argtypes = [C.c_int, C.c_int, C.c_int, _f32p, C.c_int, _f32p,
+                                      _P(C.c_double), _P(C.c_double)]
+        L.ref_objective.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), _f32p, C.c_int,
+                                    C.c_uint64, C.c_double, C.c_double, _P(C.c_double)]
         L.ref_read_mask.argtypes = [C.c_char_p, _u8p, C.c_int64, _P(C.c_int64)]
         L.ref_dynamic_select.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
                                          _P(C.c_double), C.c_int64, C.c_double, C.c_int,
@@ -214,6 +220,38 @@ class _RefLib(_Lib):
         out = (C.c_int64 * 5)()
         c = cfg.c()
         self._chk(self.lib.ref_frame_pair(nf, nt, bs, C.byref(c), i, j, out))
+        return tuple(out)
+
+    # ---- the profiler's objective (profiler.cpp:49-148) ----
+    def simulate(self, nf, nt, bs, feature_dim, seed, drift_rate=None, regime=None,
+                 spatial_scale=-1.0):
+        """proxy.cpp simulate: by drift rate, or by regime (0 Low, 1 Mid, 2 High)."""
+        n = nf * nt
+        out = np.zeros((n, feature_dim), np.float32)
+        dr = -(regime + 1.0) if regime is not None else float(drift_rate)
+        self._chk(self.lib.ref_simulate(nf, nt, bs, dr, feature_dim, spatial_scale, seed,
+                                        _fp(out)))
+        return out
+
+    def proxy_cache(self, nf, nt, bs, features, with_weights=False):
+        f = np.ascontiguousarray(features, np.float32)
+        n = f.shape[0]
+        w = np.zeros((n, n), np.float32) if with_weights else None
+        rs = np.zeros(n, np.float64)
+        sq = C.c_double()
+        self._chk(self.lib.ref_proxy_cache(nf, nt, bs, _fp(f), f.shape[1],
+                                           _fp(w) if w is not None else None,
+                                           rs.ctypes.data_as(_P(C.c_double)), C.byref(sq)))
+        return w, rs, sq.value
+
+    def objective(self, nf, nt, bs, cfg: Cfg, features, batch_seed, penalty_weight=10.0,
+                  sparsity_target=0.8):
+        """objective(c, batch, ...) -> (loss, mse, achieved_sparsity)."""
+        f = np.ascontiguousarray(features, np.float32)
+        out = (C.c_double * 3)()
+        c = cfg.c()
+        self._chk(self.lib.ref_objective(nf, nt, bs, C.byref(c), _fp(f), f.shape[1], batch_seed,
+                                         penalty_weight, sparsity_target, out))
         return tuple(out)
 
     def static_select(self, nf, nt, bs, cfg: Cfg, i, j, ratio, seed):
@@ -281,6 +319,10 @@ class _PortLib(_Lib):
         L.orc_masked_attention.argtypes = [_P(_Grid), _u8p, _f32p, _f32p, _f32p, C.c_int64,
                                            C.c_int, C.c_int, C.c_double, C.c_int64,
                                            C.c_int64, _f32p, C.c_int]
+        L.orc_proxy_cache.argtypes = [C.c_int64, C.c_int, _f32p, _f32p, _P(C.c_double),
+                                      _P(C.c_double), C.c_int]
+        L.orc_objective.argtypes = [_P(_Grid), _P(_Cfg), _f32p, C.c_int, C.c_uint64, C.c_double,
+                                    C.c_double, _P(C.c_double), C.c_int]
         L.orc_random_batch.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, _f32p, _f32p,
                                        _f32p, C.c_int]
         L.orc_mix64.argtypes = [C.c_uint64]
@@ -343,6 +385,27 @@ class _PortLib(_Lib):
 
     def masked_attention(self, nf, nt, bs, bits, q, k, v, eps=1e-10, **kw):
         return self.masked_attention_exact(nf, nt, bs, bits, q, k, v, eps=eps, **kw)
+
+    def proxy_cache(self, features, with_weights=False, threads=1):
+        f = np.ascontiguousarray(features, np.float32)
+        n = f.shape[0]
+        w = np.zeros((n, n), np.float32) if with_weights else None
+        rs = np.zeros(n, np.float64)
+        sq = C.c_double()
+        self._chk(self.lib.orc_proxy_cache(n, f.shape[1], _fp(f), _fp(w) if w is not None else None,
+                                           rs.ctypes.data_as(_P(C.c_double)), C.byref(sq),
+                                           threads))
+        return w, rs, sq.value
+
+    def objective(self, nf, nt, bs, cfg: Cfg, features, batch_seed, penalty_weight=10.0,
+                  sparsity_target=0.8, threads=1):
+        g = self._grid(nf, nt, bs)
+        f = np.ascontiguousarray(features, np.float32)
+        out = (C.c_double * 3)()
+        c = cfg.c()
+        self._chk(self.lib.orc_objective(C.byref(g), C.byref(c), _fp(f), f.shape[1], batch_seed,
+                                         penalty_weight, sparsity_target, out, threads))
+        return tuple(out)
 
     def random_batch(self, tokens, heads, d, seed, with_values=True, threads=1):
         q = np.zeros((tokens, heads, d), np.float32)

@@ -644,3 +644,145 @@ void orc_random_batch(int64_t tokens, int heads, int d, uint64_t seed,
   free(th);
   free(rs);
 }
+
+/* ---- profiler objective (profiler.cpp:49-148), SURVEY 8f3 ---------------- */
+
+typedef struct {
+  int64_t n, rb, re;
+  int dim;
+  const float* f;
+  float* w;     /* [n, n] row-major */
+  double* rs;
+} cache_t;
+
+static void* cache_run(void* arg) {
+  cache_t* a = (cache_t*)arg;
+  const int64_t n = a->n;
+  const int dim = a->dim;
+  const float scale = 1.0f / sqrtf((float)dim); /* profiler.cpp:52 (float) */
+  for (int64_t r = a->rb; r < a->re; ++r) {
+    float* wr = a->w + r * n;
+    const float* fr = a->f + r * dim;
+    /* scale * (F F^T): the float GEMM, ascending feature index */
+    for (int64_t c = 0; c < n; ++c) {
+      const float* fc = a->f + c * dim;
+      float acc = 0.0f;
+      for (int k = 0; k < dim; ++k) acc += fr[k] * fc[k];
+      wr[c] = scale * acc;
+    }
+    double m = -INFINITY;
+    for (int64_t c = 0; c < n; ++c)
+      if ((double)wr[c] > m) m = (double)wr[c];
+    double sum = 0.0;
+    for (int64_t c = 0; c < n; ++c) {
+      const double e = exp((double)wr[c] - m);
+      wr[c] = (float)e;
+      sum += e;
+    }
+    a->rs[r] = sum;
+  }
+  return NULL;
+}
+
+static void proxy_cache_fill(int64_t n, int dim, const float* f, float* w, double* rs,
+                             double* sq, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > n) threads = (int)n;
+  cache_t* as = (cache_t*)calloc((size_t)threads, sizeof(cache_t));
+  pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+  const int64_t chunk = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    cache_t* a = &as[t];
+    a->n = n; a->dim = dim; a->f = f; a->w = w; a->rs = rs;
+    a->rb = t * chunk < n ? t * chunk : n;
+    a->re = (t + 1) * chunk < n ? (t + 1) * chunk : n;
+    if (threads == 1) cache_run(a);
+    else pthread_create(&th[t], NULL, cache_run, a);
+  }
+  if (threads > 1)
+    for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  free(th);
+  free(as);
+  /* |A_dense|_F^2, sequential as profiler.cpp:70-76 */
+  double acc = 0.0;
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t c = 0; c < n; ++c) {
+      const double a = (double)w[r * n + c] / rs[r];
+      acc += a * a;
+    }
+  *sq = acc;
+}
+
+int orc_proxy_cache(int64_t tokens, int dim, const float* features, float* weights,
+                    double* row_sums, double* sq_norm, int threads) {
+  if (tokens < 1 || dim < 1) {
+    snprintf(g_err, sizeof g_err, "proxy cache: empty batch");
+    return 1;
+  }
+  float* w = weights ? weights : (float*)malloc((size_t)(tokens * tokens) * sizeof(float));
+  proxy_cache_fill(tokens, dim, features, w, row_sums, sq_norm, threads);
+  if (!weights) free(w);
+  return 0;
+}
+
+int orc_objective(const orc_grid* g, const orc_cfg* c, const float* features, int dim,
+                  uint64_t batch_seed, double penalty_weight, double sparsity_target,
+                  double* out3, int threads) {
+  const int64_t n = g->total_tokens, bs = g->block_size;
+  const uint64_t mask_seed = orc_mix64(orc_mix64(batch_seed) ^ 0x6d61736bull);
+  uint8_t* bits = (uint8_t*)calloc((size_t)(g->blocks_per_dim * g->row_bytes), 1);
+  int rc = c->mode == 1
+               ? orc_build_mask(g, c, mask_seed, 0, features, features, n, 1, dim, bits,
+                                threads, NULL)
+               : orc_build_mask(g, c, mask_seed, 0, NULL, NULL, 0, 0, 0, bits, threads, NULL);
+  if (rc) {
+    free(bits);
+    return rc;
+  }
+  float* w = (float*)malloc((size_t)(n * n) * sizeof(float));
+  double* rs = (double*)malloc((size_t)n * sizeof(double));
+  double sq = 0.0;
+  proxy_cache_fill(n, dim, features, w, rs, &sq, threads);
+  double num = 0.0;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t br = r / bs;
+    const double rd = rs[r];
+    const float* wr = w + r * n;
+    double rm = 0.0;
+    for (int64_t cb = 0; cb * bs < n; ++cb) {
+      if (!((bits[br * g->row_bytes + cb / 8] >> (cb % 8)) & 1u)) continue;
+      const int64_t hi = (cb + 1) * bs < n ? (cb + 1) * bs : n;
+      for (int64_t col = cb * bs; col < hi; ++col) rm += (double)wr[col];
+    }
+    if (rm == 0.0) {
+      for (int64_t col = 0; col < n; ++col) {
+        const double d = (double)wr[col] / rd - (col == r ? 1.0 : 0.0);
+        num += d * d;
+      }
+      continue;
+    }
+    for (int64_t cb = 0; cb * bs < n; ++cb) {
+      const int on = (bits[br * g->row_bytes + cb / 8] >> (cb % 8)) & 1u;
+      const int64_t hi = (cb + 1) * bs < n ? (cb + 1) * bs : n;
+      for (int64_t col = cb * bs; col < hi; ++col) {
+        const double x = (double)wr[col];
+        const double dense = x / rd;
+        const double d = on ? dense - x / rm : dense;
+        num += d * d;
+      }
+    }
+  }
+  int64_t active = 0;
+  for (int64_t i = 0; i < g->blocks_per_dim * g->row_bytes; ++i)
+    active += __builtin_popcount(bits[i]);
+  const double sp =
+      1.0 - (double)active / ((double)g->blocks_per_dim * (double)g->blocks_per_dim);
+  out3[1] = num / sq;
+  out3[2] = sp;
+  out3[0] = out3[1] + penalty_weight * (sparsity_target - sp > 0.0 ? sparsity_target - sp : 0.0);
+  free(w);
+  free(rs);
+  free(bits);
+  return 0;
+}
+

@@ -58,6 +58,23 @@ int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
                                int64_t row_begin, int64_t row_end, float* out,
                                int threads);
 
+/* masked_attention (attention.cpp:59-81, 107-113): soft mask, eps > 0. */
+int orc_masked_attention(const orc_grid* g, const uint8_t* bits, const float* q,
+                         const float* k, const float* v, int64_t tokens, int heads, int d,
+                         double eps, int64_t row_begin, int64_t row_end, float* out,
+                         int threads);
+
+/* build_proxy_cache (profiler.cpp:49-78): features [S, dim] row-major;
+ * weights [S, S] row-major (may be NULL: not stored), row_sums [S]. */
+int orc_proxy_cache(int64_t tokens, int dim, const float* features, float* weights,
+                    double* row_sums, double* sq_norm, int threads);
+
+/* objective (profiler.cpp:80-148) with its own cache: out3 = {loss, mse,
+ * achieved_sparsity}.  features: ProxyBatch::features [total_tokens, dim]. */
+int orc_objective(const orc_grid* g, const orc_cfg* c, const float* features, int dim,
+                  uint64_t batch_seed, double penalty_weight, double sparsity_target,
+                  double* out3, int threads);
+
 /* random_batch (attention.cpp:182-204): [tokens, heads, d] each. */
 void orc_random_batch(int64_t tokens, int heads, int d, uint64_t seed,
                       float* q, float* k, float* v, int threads);

@@ -20,6 +20,8 @@
 #include "oracle.hpp"
 #include "radialplan/attention.hpp"
 #include "radialplan/mask.hpp"
+#include "radialplan/profiler.hpp"
+#include "radialplan/proxy.hpp"
 #include "radialplan/radial.hpp"
 #include "radialplan/selection.hpp"
 
@@ -308,6 +310,67 @@ int ref_read_mask(const char* path, std::uint8_t* bits, std::int64_t cap, std::i
     if (static_cast<std::int64_t>(m.bits.size()) > cap)
       throw std::out_of_range("ref_read_mask: capacity");
     std::memcpy(bits, m.bits.data(), m.bits.size());
+  });
+}
+
+// ---- the profiler's per-trial objective (profiler.cpp:49-148) --
+
+// simulate (proxy.hpp:36-39): drift_rate < 0 selects a regime preset
+// (regime = -drift_rate - 1: 0 Low, 1 Mid, 2 High).  features out:
+// [total_tokens, feature_dim] row-major.
+int ref_simulate(int nf, int nt, int bs, double drift_rate, int feature_dim,
+                 double spatial_scale, std::uint64_t seed, float* features) {
+  return guarded([&] {
+    const GridSpec g = make_grid(nf, nt, bs);
+    const ProxyBatch b =
+        drift_rate < 0 ? simulate(static_cast<Regime>(static_cast<int>(-drift_rate) - 1), g,
+                                  feature_dim, spatial_scale, seed)
+                       : simulate(drift_rate, g, feature_dim, spatial_scale, seed);
+    for (std::int64_t t = 0; t < g.total_tokens; ++t)
+      for (int d = 0; d < feature_dim; ++d) features[t * feature_dim + d] = b.features(t, d);
+  });
+}
+
+namespace {
+ProxyBatch proxy_batch(int nf, int nt, int bs, const float* features, int feature_dim,
+                       std::uint64_t seed) {
+  ProxyBatch b;
+  b.grid = make_grid(nf, nt, bs);
+  b.feature_dim = feature_dim;
+  b.seed = seed;
+  b.features.resize(b.grid.total_tokens, feature_dim);
+  for (std::int64_t t = 0; t < b.grid.total_tokens; ++t)
+    for (int d = 0; d < feature_dim; ++d) b.features(t, d) = features[t * feature_dim + d];
+  return b;
+}
+}  // namespace
+
+// build_proxy_cache: weights [n, n] row-major (or NULL), row_sums [n],
+// reference_sq_norm [1].
+int ref_proxy_cache(int nf, int nt, int bs, const float* features, int feature_dim,
+                    float* weights, double* row_sums, double* sq_norm) {
+  return guarded([&] {
+    const ProxyBatch b = proxy_batch(nf, nt, bs, features, feature_dim, 0);
+    const DenseProxyCache c = build_proxy_cache(b);
+    const std::int64_t n = b.grid.total_tokens;
+    if (weights)
+      for (std::int64_t r = 0; r < n; ++r)
+        for (std::int64_t col = 0; col < n; ++col) weights[r * n + col] = c.weights(r, col);
+    for (std::int64_t r = 0; r < n; ++r) row_sums[r] = c.row_sums[static_cast<std::size_t>(r)];
+    *sq_norm = c.reference_sq_norm;
+  });
+}
+
+// objective (with its own cache): out3 = {loss, mse, achieved_sparsity}.
+int ref_objective(int nf, int nt, int bs, const ref_cfg* cfg, const float* features,
+                  int feature_dim, std::uint64_t batch_seed, double penalty_weight,
+                  double sparsity_target, double* out3) {
+  return guarded([&] {
+    const ProxyBatch b = proxy_batch(nf, nt, bs, features, feature_dim, batch_seed);
+    const TrialRecord r = objective(to_cfg(cfg), b, penalty_weight, sparsity_target, nullptr);
+    out3[0] = r.loss;
+    out3[1] = r.mse;
+    out3[2] = r.achieved_sparsity;
   });
 }
 

@@ -102,6 +102,10 @@ class BuildOptions(C.Structure):
     ]
 
 
+class Trial(C.Structure):
+    _fields_ = [("loss", C.c_double), ("mse", C.c_double), ("achieved_sparsity", C.c_double)]
+
+
 class BuildStats(C.Structure):
     _fields_ = [
         ("retained_frame_pairs", C.c_int64),
@@ -155,6 +159,12 @@ _SIGS = {
                                C.c_double, C.c_float, _v], C.c_int),
     "rp_masked_attention_host": ([_P(Grid), _v, _v, _v, _v, C.c_int, C.c_int64, C.c_int,
                                   C.c_int, C.c_double, _v, _v], C.c_int),
+    "rp_proxy_cache_create": ([_P(Grid), _v, C.c_int, _P(_v), _v], C.c_int),
+    "rp_proxy_cache_from_weights": ([_P(Grid), _v, _v, C.c_double, _P(_v), _v], C.c_int),
+    "rp_proxy_cache_destroy": ([_v], None),
+    "rp_proxy_cache_stats": ([_v, _v, _P(C.c_double), _v], C.c_int),
+    "rp_objective": ([_v, _P(Config), C.c_uint64, _v, C.c_int, C.c_double, C.c_double,
+                      _P(Trial), _v, _v], C.c_int),
     "rp_static_select": ([_P(Band), C.c_double, C.c_uint64, _v, C.c_int64, _P(C.c_int64), _v],
                          C.c_int),
     "rp_proxy_scores": ([_P(Tensor), _P(Tensor), C.c_int, _P(Band), _v, _v], C.c_int),

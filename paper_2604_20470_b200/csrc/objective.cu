@@ -1,0 +1,545 @@
+// the profiler's per-trial objective on the GPU
+// (build_proxy_cache, profiler.cpp:49-78; objective, profiler.cpp:80-148).
+//
+// The reference caches the dense proxy attention -- an S x S float matrix of
+// softmax numerators exp(logit - row max) -- and every trial re-weights it by
+// the trial's block mask: two full passes over S^2 floats.  Everything a
+// trial needs from that matrix is a per-(row, column block) statistic, so the
+// B200 cache keeps only
+//   s1[r][cb] = sum_{col in cb, col < S} w[r, col]
+//   s2[r][cb] = sum_{col in cb, col < S} w[r, col]^2        (double)
+//   diag[r]   = w[r, r],  row_sums[r] (the reference's double sums of exp),
+//   reference_sq_norm = sum_r sum_c (w[r, c] / row_sums[r])^2
+// (S x ceil(S/B) x 16 bytes: 715 MB instead of 22.8 GB at the Wan shape), and
+// a trial reads only S x ceil(S/B) statistics:
+//   rs_mask = sum_{active cb} s1,
+//   num_r   = sum_{inactive} s2 / rd^2 + (1/rd - 1/rs_mask)^2 sum_{active} s2
+//   (exactly the reference's sum over (w/rd - w/rs_mask)^2 and (w/rd)^2,
+//   factored; rs_mask == 0 takes the reference's point-mass fallback).
+//
+// Arithmetic contract: the logits are the reference's float GEMM evaluated in
+// its order (ascending feature index, separate rounded multiply and add, as
+// the Eigen-subset build of oracle/_ref and an FMA-free x86 build compute
+// them), scaled by the float 1/sqrt(dim); exp in double; weights rounded to
+// float, row sums of the unrounded doubles (profiler.cpp:60-68).  Sums run in
+// a fixed parallel order (deterministic; ~1e-16 relative from the sequential
+// order), so mse agrees with the reference to ~1e-12 relative except where
+// rs_mask ~ rd makes (1/rd - 1/rs_mask) cancel in both.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+#include "plan.hpp"
+
+struct rp_proxy_cache {
+  rp_grid g;
+  int64_t n;    // real tokens S
+  int64_t nbr;  // column blocks touching real tokens, ceil(S / B)
+  double* s1 = nullptr;
+  double* s2 = nullptr;
+  float* diag = nullptr;
+  double* row_sums = nullptr;
+  double* sq = nullptr;  // [1]
+};
+
+namespace rp {
+namespace objective {
+
+constexpr int kT = 64;        // tile rows / columns
+constexpr int kKC = 32;       // feature-index chunk staged in shared memory
+constexpr int kThreads = 256; // 16 x 16 threads, 4 x 4 logits each
+
+// Ordered-int encoding of floats for atomicMax.
+RP_DEV int f2key(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+RP_DEV float key2f(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF); }
+
+struct Split {
+  int64_t c_begin, c_end;  // columns [c_begin, c_end) of this CTA (block-aligned)
+};
+
+// Columns of split j: units of U = max(B, 64) columns, split evenly.
+RP_DEV Split split_of(int64_t n, int64_t unit, int splits, int j) {
+  const int64_t units = (n + unit - 1) / unit;
+  Split s;
+  s.c_begin = units * j / splits * unit;
+  s.c_end = min(n, units * (j + 1) / splits * unit);
+  return s;
+}
+
+// acc[i][j] = scale * sum_k F[r0 + 4ty + i][k] * F[c0 + 4tx + j][k], the
+// reference's float GEMM order (k ascending, rounded multiply then add).
+RP_DEV void logits_tile(const float* __restrict__ F, int64_t n, int dim, int64_t r0, int64_t c0,
+                        float scale, float (&fr)[kKC][kT + 4], float (&fc)[kKC][kT + 4],
+                        float (&acc)[4][4]) {
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < dim; k0 += kKC) {
+    const int kc = min(kKC, dim - k0);
+    __syncthreads();
+    for (int idx = tid; idx < kT * kKC; idx += kThreads) {
+      const int row = idx / kKC, k = idx % kKC;
+      const int64_t gr = r0 + row, gc = c0 + row;
+      fr[k][row] = (k < kc && gr < n) ? F[gr * dim + k0 + k] : 0.f;
+      fc[k][row] = (k < kc && gc < n) ? F[gc * dim + k0 + k] : 0.f;
+    }
+    __syncthreads();
+    for (int k = 0; k < kc; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&fr[k][4 * ty]);
+      const float4 b = *reinterpret_cast<const float4*>(&fc[k][4 * tx]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = __fmul_rn(scale, acc[i][j]);
+}
+
+// Pass 1: row max of the logits (blockIdx.x: 64-row tile, blockIdx.y: split).
+__global__ void __launch_bounds__(kThreads) rowmax_kernel(const float* __restrict__ F, int64_t n,
+                                                          int dim, float scale, int64_t unit,
+                                                          int* __restrict__ max_key) {
+  __shared__ __align__(16) float fr[kKC][kT + 4];
+  __shared__ __align__(16) float fc[kKC][kT + 4];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kT;
+  const Split sp = split_of(n, unit, gridDim.y, blockIdx.y);
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int64_t c0 = sp.c_begin; c0 < sp.c_end; c0 += kT) {
+    float acc[4][4];
+    logits_tile(F, n, dim, r0, c0, scale, fr, fc, acc);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c0 + 4 * tx + j < sp.c_end) mx[i] = fmaxf(mx[i], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xFFFFFFFFu, mx[i], o));
+    const int64_t r = r0 + 4 * ty + i;
+    if (tx == 0 && r < n && sp.c_end > sp.c_begin) atomicMax(max_key + r, f2key(mx[i]));
+  }
+}
+
+// Pass 2: w = float(exp(double(logit) - m_r)); per-(row, block) sums of w and
+// w^2, the diagonal, and per-(row, split) sums of the double exponentials.
+// FROM_W: w is read from a given weights matrix (row-major S x S) instead.
+template <bool FROM_W>
+__global__ void __launch_bounds__(kThreads)
+    partials_kernel(const float* __restrict__ F, const float* __restrict__ W, int64_t n, int dim,
+                    float scale, int block, int64_t unit, int64_t nbr,
+                    const int* __restrict__ max_key, double* __restrict__ s1,
+                    double* __restrict__ s2, float* __restrict__ diag,
+                    double* __restrict__ rs_part) {
+  __shared__ __align__(16) float fr[kKC][kT + 4];
+  __shared__ __align__(16) float fc[kKC][kT + 4];
+  __shared__ float E[kT][kT + 1];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kT;
+  const Split sp = split_of(n, unit, gridDim.y, blockIdx.y);
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  double m[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + 4 * ty + i;
+    m[i] = (!FROM_W && r < n) ? static_cast<double>(key2f(max_key[r])) : 0.0;
+  }
+  double rsum[4] = {0.0, 0.0, 0.0, 0.0};
+  // walk phase: thread -> (row wr, 16-column segment q)
+  const int wr = tid / 4, q = tid % 4;
+  const int64_t grow = r0 + wr;
+  double run1 = 0.0, run2 = 0.0;  // block running sums when B > 64 (q == 0)
+  for (int64_t c0 = sp.c_begin; c0 < sp.c_end; c0 += kT) {
+    if constexpr (!FROM_W) {
+      float acc[4][4];
+      logits_tile(F, n, dim, r0, c0, scale, fr, fc, acc);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t r = r0 + 4 * ty + i, c = c0 + 4 * tx + j;
+          float w = 0.f;
+          if (r < n && c < sp.c_end) {
+            const double e = exp(static_cast<double>(acc[i][j]) - m[i]);
+            rsum[i] += e;
+            w = static_cast<float>(e);
+            if (c == r) diag[r] = w;
+          }
+          E[4 * ty + i][4 * tx + j] = w;
+        }
+    } else {
+      __syncthreads();
+      for (int idx = tid; idx < kT * kT; idx += kThreads) {
+        const int i = idx / kT, j = idx % kT;
+        const int64_t r = r0 + i, c = c0 + j;
+        const float w = (r < n && c < sp.c_end) ? W[r * n + c] : 0.f;
+        E[i][j] = w;
+        if (r < n && c == r) diag[r] = w;
+      }
+    }
+    __syncthreads();
+    // per-block sums along the row (fixed order)
+    double a1 = 0.0, a2 = 0.0;
+    const int64_t cs = c0 + 16 * q;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const double w = E[wr][16 * q + i];
+      a1 += w;
+      a2 += w * w;
+      if (block < 16 && ((cs + i + 1) % block == 0 || cs + i + 1 == sp.c_end)) {
+        if (grow < n && cs + i < sp.c_end) {
+          const int64_t cb = (cs + i) / block;
+          s1[grow * nbr + cb] = a1;
+          s2[grow * nbr + cb] = a2;
+        }
+        a1 = a2 = 0.0;
+      }
+    }
+    if (block >= 16) {
+      if (block >= 32) {
+        a1 += __shfl_xor_sync(0xFFFFFFFFu, a1, 1);
+        a2 += __shfl_xor_sync(0xFFFFFFFFu, a2, 1);
+      }
+      if (block >= 64) {
+        a1 += __shfl_xor_sync(0xFFFFFFFFu, a1, 2);
+        a2 += __shfl_xor_sync(0xFFFFFFFFu, a2, 2);
+      }
+      const int lanes = block >= 64 ? 4 : block / 16;  // segments per block in this tile
+      if (q % lanes == 0 && grow < n && cs < sp.c_end) {
+        if (block <= 64) {
+          const int64_t cb = cs / block;
+          s1[grow * nbr + cb] = a1;
+          s2[grow * nbr + cb] = a2;
+        } else {
+          run1 += a1;
+          run2 += a2;
+          const int64_t next = c0 + kT;
+          if (next % block == 0 || next >= sp.c_end) {
+            const int64_t cb = c0 / block;
+            s1[grow * nbr + cb] = run1;
+            s2[grow * nbr + cb] = run2;
+            run1 = run2 = 0.0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if constexpr (!FROM_W) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) rsum[i] += __shfl_xor_sync(0xFFFFFFFFu, rsum[i], o);
+      const int64_t r = r0 + 4 * ty + i;
+      if (tx == 0 && r < n) rs_part[r * gridDim.y + blockIdx.y] = rsum[i];
+    }
+  }
+}
+
+// Per row: row sum (ordered over splits) and its share of |A_dense|_F^2.
+__global__ void rows_kernel(int64_t n, int splits, int64_t nbr, const double* __restrict__ rs_part,
+                            const double* __restrict__ s2, double* __restrict__ row_sums,
+                            double* __restrict__ sq_part, bool have_sums) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double rs;
+  if (have_sums) {
+    rs = row_sums[r];
+  } else {
+    rs = 0.0;
+    for (int j = 0; j < splits; ++j) rs += rs_part[r * splits + j];
+    row_sums[r] = rs;
+  }
+  double t2 = 0.0;
+  for (int64_t cb = 0; cb < nbr; ++cb) t2 += s2[r * nbr + cb];
+  sq_part[r] = t2 / rs / rs;
+}
+
+// Deterministic sum of x[0..n) (one CTA of 1024 threads).
+__global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ x, int64_t n,
+                                                   double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) a += x[i];
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = 512; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// One warp per real row: the trial's reconstruction error for that row
+// (profiler.cpp:110-140), from the cached block statistics.
+__global__ void trial_kernel(int64_t n, int block, int64_t nbr, int64_t row_bytes,
+                             const uint8_t* __restrict__ bits, const double* __restrict__ s1,
+                             const double* __restrict__ s2, const float* __restrict__ diag,
+                             const double* __restrict__ row_sums, double* __restrict__ num) {
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= n) return;
+  const int64_t br = r / block;
+  double a1 = 0.0, b2 = 0.0, c2 = 0.0;
+  for (int64_t cb = lane; cb < nbr; cb += 32) {
+    const bool on = (bits[br * row_bytes + cb / 8] >> (cb % 8)) & 1u;
+    const double x1 = s1[r * nbr + cb], x2 = s2[r * nbr + cb];
+    if (on) {
+      a1 += x1;
+      b2 += x2;
+    } else {
+      c2 += x2;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a1 += __shfl_xor_sync(0xFFFFFFFFu, a1, o);
+    b2 += __shfl_xor_sync(0xFFFFFFFFu, b2, o);
+    c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
+  }
+  if (lane) return;
+  const double rd = row_sums[r];
+  double v;
+  if (a1 == 0.0) {
+    // fully masked row: the sparse row is a point mass on the diagonal
+    const double d = diag[r];
+    const double t = d / rd - 1.0;
+    v = (b2 + c2 - d * d) / (rd * rd) + t * t;
+  } else {
+    const double f = 1.0 / rd - 1.0 / a1;
+    v = c2 / (rd * rd) + b2 * f * f;
+  }
+  num[r] = v;
+}
+
+struct Geometry {
+  int64_t unit;
+  int row_tiles, splits;
+};
+
+Geometry geometry(int64_t n, int block) {
+  Geometry g;
+  g.unit = std::max<int64_t>(block, kT);
+  g.row_tiles = static_cast<int>((n + kT - 1) / kT);
+  const int64_t units = (n + g.unit - 1) / g.unit;
+  const int64_t want = (2 * 148 + g.row_tiles - 1) / g.row_tiles;
+  g.splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, want)));
+  return g;
+}
+
+template <class T>
+T* dalloc(size_t count, cudaStream_t s) {
+  T* p = nullptr;
+  RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+  return p;
+}
+
+rp_proxy_cache* new_cache(const rp_grid& g, cudaStream_t s) {
+  auto* c = new rp_proxy_cache;
+  c->g = g;
+  c->n = g.total_tokens;
+  c->nbr = (c->n + g.block_size - 1) / g.block_size;
+  c->s1 = dalloc<double>(static_cast<size_t>(c->n * c->nbr), s);
+  c->s2 = dalloc<double>(static_cast<size_t>(c->n * c->nbr), s);
+  c->diag = dalloc<float>(static_cast<size_t>(c->n), s);
+  c->row_sums = dalloc<double>(static_cast<size_t>(c->n), s);
+  c->sq = dalloc<double>(1, s);
+  return c;
+}
+
+void free_cache(rp_proxy_cache* c, cudaStream_t s) {
+  if (!c) return;
+  for (void* p : {static_cast<void*>(c->s1), static_cast<void*>(c->s2),
+                  static_cast<void*>(c->diag), static_cast<void*>(c->row_sums),
+                  static_cast<void*>(c->sq)})
+    if (p) cudaFreeAsync(p, s);
+  delete c;
+}
+
+// Shared tail: row sums / squared norm from the block statistics.
+void finish_cache(rp_proxy_cache* c, const double* rs_part, int splits, bool have_sums,
+                  cudaStream_t s) {
+  double* sq_part = dalloc<double>(static_cast<size_t>(c->n), s);
+  rows_kernel<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, s>>>(
+      c->n, splits, c->nbr, rs_part, c->s2, c->row_sums, sq_part, have_sums);
+  RP_LAUNCHED();
+  sum_kernel<<<1, 1024, 0, s>>>(sq_part, c->n, c->sq);
+  RP_LAUNCHED();
+  RP_CUDA(cudaFreeAsync(sq_part, s));
+}
+
+}  // namespace objective
+}  // namespace rp
+
+using namespace rp;
+using namespace rp::objective;
+
+extern "C" {
+
+rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev, int feature_dim,
+                                rp_proxy_cache** out, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    if (!out) throw std::invalid_argument("proxy cache: null output");
+    if (!features_dev) throw std::invalid_argument("proxy cache: null features");
+    if (feature_dim < 1) throw std::invalid_argument("proxy cache: feature_dim must be >= 1");
+    *out = nullptr;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    rp_proxy_cache* c = new_cache(*g, s);
+    try {
+      const int64_t n = c->n;
+      const Geometry geo = geometry(n, g->block_size);
+      // profiler.cpp:52: float scale = 1.0f / sqrt(float(cols))
+      const float scale = 1.0f / std::sqrt(static_cast<float>(feature_dim));
+      int* keys = dalloc<int>(static_cast<size_t>(n), s);
+      double* rs_part = dalloc<double>(static_cast<size_t>(n) * geo.splits, s);
+      std::vector<int> init(static_cast<size_t>(n), INT_MIN);
+      RP_CUDA(cudaMemcpyAsync(keys, init.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+      const dim3 grid(static_cast<unsigned>(geo.row_tiles), static_cast<unsigned>(geo.splits));
+      rowmax_kernel<<<grid, kThreads, 0, s>>>(features_dev, n, feature_dim, scale, geo.unit, keys);
+      RP_LAUNCHED();
+      partials_kernel<false><<<grid, kThreads, 0, s>>>(
+          features_dev, nullptr, n, feature_dim, scale, g->block_size, geo.unit, c->nbr, keys,
+          c->s1, c->s2, c->diag, rs_part);
+      RP_LAUNCHED();
+      finish_cache(c, rs_part, geo.splits, false, s);
+      RP_CUDA(cudaFreeAsync(keys, s));
+      RP_CUDA(cudaFreeAsync(rs_part, s));
+      RP_CUDA(cudaStreamSynchronize(s));  // init[] is pageable host memory
+    } catch (...) {
+      free_cache(c, s);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+rp_status rp_proxy_cache_from_weights(const rp_grid* g, const float* weights_dev,
+                                      const double* row_sums_dev, double reference_sq_norm,
+                                      rp_proxy_cache** out, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    if (!out || !weights_dev || !row_sums_dev)
+      throw std::invalid_argument("proxy cache: null buffer");
+    *out = nullptr;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    rp_proxy_cache* c = new_cache(*g, s);
+    try {
+      const Geometry geo = geometry(c->n, g->block_size);
+      RP_CUDA(cudaMemcpyAsync(c->row_sums, row_sums_dev, sizeof(double) * c->n,
+                              cudaMemcpyDeviceToDevice, s));
+      const dim3 grid(static_cast<unsigned>(geo.row_tiles), static_cast<unsigned>(geo.splits));
+      partials_kernel<true><<<grid, kThreads, 0, s>>>(nullptr, weights_dev, c->n, 0, 0.f,
+                                                      g->block_size, geo.unit, c->nbr, nullptr,
+                                                      c->s1, c->s2, c->diag, nullptr);
+      RP_LAUNCHED();
+      // the caller's squared norm is kept as given (profiler.cpp:142 divides by it)
+      RP_CUDA(cudaMemcpyAsync(c->sq, &reference_sq_norm, sizeof(double), cudaMemcpyHostToDevice, s));
+      RP_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      free_cache(c, s);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void rp_proxy_cache_destroy(rp_proxy_cache* c) {
+  if (!c) return;
+  cudaStreamSynchronize(nullptr);
+  free_cache(c, nullptr);
+  cudaStreamSynchronize(nullptr);
+}
+
+rp_status rp_proxy_cache_stats(const rp_proxy_cache* c, double* row_sums_host,
+                               double* reference_sq_norm, rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (!c) throw std::invalid_argument("proxy cache: null");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (row_sums_host)
+      RP_CUDA(cudaMemcpyAsync(row_sums_host, c->row_sums, sizeof(double) * c->n,
+                              cudaMemcpyDeviceToHost, s));
+    if (reference_sq_norm)
+      RP_CUDA(cudaMemcpyAsync(reference_sq_norm, c->sq, sizeof(double), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+rp_status rp_objective(const rp_proxy_cache* cache, const rp_config* cfg, uint64_t batch_seed,
+                       const float* features_dev, int feature_dim, double penalty_weight,
+                       double sparsity_target, rp_trial* out, uint8_t* mask_bits_dev,
+                       rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (!cache || !cfg || !out) throw std::invalid_argument("objective: null argument");
+    plan::validate(*cfg);  // c.validate() (profiler.cpp:83)
+    const rp_grid& g = cache->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nb = g.blocks_per_dim;
+    uint8_t* bits = mask_bits_dev;
+    uint8_t* own = nullptr;
+    if (!bits) {
+      own = dalloc<uint8_t>(static_cast<size_t>(nb * g.row_bytes), s);
+      bits = own;
+    }
+    struct Guard {
+      uint8_t* p;
+      cudaStream_t s;
+      ~Guard() {
+        if (p) cudaFreeAsync(p, s);
+      }
+    } guard{own, s};
+    // mask seed mix64(batch.seed, "mask") (profiler.cpp:91); dynamic mode
+    // scores scoring_features(batch): one fused head of the whole feature row
+    const uint64_t seed = mix64(mix64(batch_seed) ^ 0x6d61736bull);
+    rp_status st;
+    if (cfg->mode == RP_DYNAMIC_THRESHOLD) {
+      if (!features_dev || feature_dim < 1)
+        throw std::invalid_argument("objective: dynamic mode needs the batch features");
+      rp_tensor f{const_cast<float*>(features_dev), RP_F32, cache->n, 1, feature_dim,
+                  feature_dim, feature_dim};
+      st = rp_build_mask(&g, cfg, seed, nullptr, &f, &f, 1, bits, nullptr, stream);
+    } else {
+      st = rp_build_mask(&g, cfg, seed, nullptr, nullptr, nullptr, 0, bits, nullptr, stream);
+    }
+    if (st != RP_OK) throw CudaError(std::string("objective: build_mask: ") + rp_last_error());
+    double* num = dalloc<double>(static_cast<size_t>(cache->n) + 1, s);
+    trial_kernel<<<static_cast<unsigned>((cache->n * 32 + 255) / 256), 256, 0, s>>>(
+        cache->n, g.block_size, cache->nbr, g.row_bytes, bits, cache->s1, cache->s2, cache->diag,
+        cache->row_sums, num);
+    RP_LAUNCHED();
+    sum_kernel<<<1, 1024, 0, s>>>(num, cache->n, num + cache->n);
+    RP_LAUNCHED();
+    double h[2] = {0.0, 0.0};
+    RP_CUDA(cudaMemcpyAsync(&h[0], num + cache->n, sizeof(double), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaMemcpyAsync(&h[1], cache->sq, sizeof(double), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaFreeAsync(num, s));
+    int64_t active = 0;
+    double sparsity = 0.0;
+    st = rp_mask_sparsity(&g, bits, &active, &sparsity, stream);  // synchronizes s
+    if (st != RP_OK) throw CudaError(std::string("objective: sparsity: ") + rp_last_error());
+    out->mse = h[0] / h[1];
+    out->achieved_sparsity = sparsity;
+    out->loss = out->mse + penalty_weight * std::max(0.0, sparsity_target - sparsity);
+  });
+}
+
+}  // extern "C"

@@ -673,6 +673,77 @@ def masked_attention(g: GridSpec, mask: BlockMask, q: np.ndarray, k: np.ndarray,
                            C.c_double(epsilon))
 
 
+# ------------------------------------------- profiler objective --
+class ProxyCache:
+    """build_proxy_cache (profiler.cpp:49-78) on the GPU, device-resident.
+
+    features: the ProxyBatch features, float32 [total_tokens, feature_dim]
+    CUDA tensor.  Keeps per-(row, column block) statistics of the dense proxy
+    attention instead of the S x S matrix (rp_proxy_cache_create)."""
+
+    def __init__(self, g: GridSpec, features=None, *, _handle=None, stream=None):
+        self.grid = g
+        self._h = _handle
+        if self._h is None:
+            torch = _torch()
+            f = features.contiguous()
+            if f.dtype != torch.float32 or not f.is_cuda or f.dim() != 2:
+                raise InvalidArgument("proxy cache: features must be a float32 [S, dim] CUDA tensor")
+            h = C.c_void_p()
+            gc = g.c()
+            L.check(L.lib().rp_proxy_cache_create(C.byref(gc), C.c_void_p(f.data_ptr()),
+                                                  f.shape[1], C.byref(h), _stream(stream)))
+            self._h = h
+
+    @classmethod
+    def from_weights(cls, g: GridSpec, weights, row_sums, reference_sq_norm: float, stream=None):
+        """From a reference-layout cache: weights [S, S] float32 and row_sums
+        [S] float64 CUDA tensors (rp_proxy_cache_from_weights)."""
+        h = C.c_void_p()
+        gc = g.c()
+        w, rs = weights.contiguous(), row_sums.contiguous()
+        L.check(L.lib().rp_proxy_cache_from_weights(C.byref(gc), C.c_void_p(w.data_ptr()),
+                                                    C.c_void_p(rs.data_ptr()),
+                                                    float(reference_sq_norm), C.byref(h),
+                                                    _stream(stream)))
+        return cls(g, _handle=h)
+
+    def stats(self):
+        """(row_sums [S] float64, reference_sq_norm)."""
+        rs = np.zeros(self.grid.total_tokens, np.float64)
+        sq = C.c_double()
+        L.check(L.lib().rp_proxy_cache_stats(self._h, rs.ctypes.data_as(C.c_void_p),
+                                             C.byref(sq), None))
+        return rs, sq.value
+
+    def objective(self, c: SparsityConfig, batch_seed: int, features=None,
+                  penalty_weight: float = 10.0, sparsity_target: float = 0.80, mask_out=None,
+                  stream=None):
+        """objective (profiler.cpp:80-148): (loss, mse, achieved_sparsity).
+        Dynamic configs need the batch features (scored as one fused head)."""
+        t = L.Trial()
+        cc = c.c()
+        fp, dim = None, 0
+        if features is not None:
+            fp, dim = C.c_void_p(features.data_ptr()), features.shape[1]
+        L.check(L.lib().rp_objective(self._h, C.byref(cc), batch_seed, fp, dim,
+                                     penalty_weight, sparsity_target, C.byref(t),
+                                     C.c_void_p(mask_out.data_ptr()) if mask_out is not None
+                                     else None, _stream(stream)))
+        return t.loss, t.mse, t.achieved_sparsity
+
+    def close(self):
+        if self._h:
+            L.lib().rp_proxy_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class PooledMode(enum.IntEnum):
     TopK = 0   # static ratio: keep max(1, floor(ratio * n)) best candidates per block row
     Mass = 1   # dynamic: smallest best-first prefix reaching a softmax mass

@@ -134,3 +134,33 @@ def test_soft_attention_restatement_vs_reference_golden(port):
         assert np.abs(out - want).max() <= 1e-6, eps
     with pytest.raises(pyoracle.OracleError):
         port.masked_attention(nf, nt, bs, z["bits"], q, k, v, eps=0.0)
+
+
+def test_objective_restatement_vs_reference_golden(port):
+    """build_proxy_cache / objective (profiler.cpp:49-148): the C restatement
+    reproduces the reference's golden records bit for bit."""
+    z = np.load(f"{GOLDEN}/objective.npz")
+    nf, nt, bs = int(z["nf"]), int(z["nt"]), int(z["bs"])
+    for r, seed in enumerate(z["seeds"]):
+        f = z["features"][r]
+        _, rs, sq = port.proxy_cache(f, threads=2)
+        assert np.array_equal(rs, z["row_sums"][r]) and sq == z["sq_norm"][r]
+        for c, want in zip(z["configs"], z["trials"][r]):
+            cfg = Cfg(int(c[0]), *c[1:8], int(c[8]))
+            got = port.objective(nf, nt, bs, cfg, f, int(seed), threads=2)
+            assert got == tuple(want), (r, c)
+
+
+def test_objective_restatement_vs_reference_random(ref, port):
+    """Fresh simulated batches and configs, straight against oracle/_ref."""
+    rng = np.random.default_rng(3)
+    for trial in range(6):
+        nf, nt, bs = 5, 64, (8, 16, 32)[trial % 3]
+        f = ref.simulate(nf, nt, bs, 24, 100 + trial, drift_rate=float(rng.uniform(0, 0.5)))
+        mode = trial % 2
+        far = float(rng.uniform(-1, 2)) if mode else float(rng.uniform(0.1, 0.8))
+        cfg = Cfg(mode, float(rng.uniform(1, 3)), float(rng.uniform(0.1, 1)), 1e-6,
+                  float(rng.uniform(0.1, 1)), float(rng.uniform(0.1, 1)),
+                  float(rng.uniform(-1, 1)) if mode else float(rng.uniform(0.3, 1)), far, 1)
+        want = ref.objective(nf, nt, bs, cfg, f, 7 + trial)
+        assert port.objective(nf, nt, bs, cfg, f, 7 + trial, threads=2) == want
