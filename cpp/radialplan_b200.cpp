@@ -647,4 +647,136 @@ void sparse_attention(const GridSpec& g, const DeviceTensor& q, const DeviceTens
 }
 
 }  // namespace b200
+
+// ------------------------------------------------- profiler objective (8f3) --
+namespace {
+// ProxyBatch::features (column-major host) -> [S, dim] row-major f32.
+std::vector<float> pack_features(const ProxyBatch& b) {
+  const std::int64_t n = b.features.rows();
+  const int d = static_cast<int>(b.features.cols());
+  if (n != b.grid.total_tokens || d != b.feature_dim || d < 1)
+    throw std::invalid_argument("proxy batch: features must be total_tokens x feature_dim");
+  std::vector<float> f(static_cast<std::size_t>(n) * d);
+  for (std::int64_t t = 0; t < n; ++t)
+    for (int k = 0; k < d; ++k) f[static_cast<std::size_t>(t) * d + k] = b.features(t, k);
+  return f;
+}
+
+TrialRecord run_objective(const rp_proxy_cache* cache, const SparsityConfig& c,
+                          std::uint64_t seed, const float* features_dev, int dim,
+                          double penalty_weight, double sparsity_target) {
+  const rp_config cc = b200::to_c(c);
+  rp_trial t{};
+  check(rp_objective(cache, &cc, seed, features_dev, dim, penalty_weight, sparsity_target, &t,
+                     nullptr, nullptr));
+  TrialRecord r;
+  r.config = c;
+  r.loss = t.loss;
+  r.mse = t.mse;
+  r.achieved_sparsity = t.achieved_sparsity;
+  return r;
+}
+}  // namespace
+
+FeatureBatch scoring_features(const ProxyBatch& batch, int fused_heads) {
+  if (fused_heads < 1) throw std::invalid_argument("scoring_features: fused_heads must be >= 1");
+  if (batch.feature_dim % fused_heads != 0)
+    throw std::invalid_argument("scoring_features: feature_dim not divisible by fused_heads");
+  FeatureBatch f;
+  f.tokens = batch.features.rows();
+  f.heads = fused_heads;
+  f.head_dim = batch.feature_dim / fused_heads;
+  for (int h = 0; h < fused_heads; ++h) {
+    Eigen::MatrixXf slice = batch.features.middleCols(static_cast<Eigen::Index>(h) * f.head_dim,
+                                                      f.head_dim);
+    f.queries.push_back(slice);
+    f.keys.push_back(std::move(slice));
+  }
+  return f;
+}
+
+DenseProxyCache build_proxy_cache(const ProxyBatch& batch) {
+  const std::vector<float> f = pack_features(batch);
+  const std::int64_t n = batch.grid.total_tokens;
+  const rp_grid gc = b200::to_c(batch.grid);
+  DeviceArray<float> df(f.size());
+  df.put(f.data(), f.size());
+  DeviceArray<float> dw(static_cast<std::size_t>(n * n));
+  DeviceArray<double> drs(static_cast<std::size_t>(n));
+  DenseProxyCache c;
+  check(rp_proxy_weights(&gc, df.get(), batch.feature_dim, dw.get(), drs.get(),
+                         &c.reference_sq_norm, nullptr));
+  std::vector<float> w(static_cast<std::size_t>(n * n));
+  dw.get_to(w.data(), w.size());
+  c.row_sums.resize(static_cast<std::size_t>(n));
+  drs.get_to(c.row_sums.data(), c.row_sums.size());
+  c.weights = Eigen::MatrixXf(n, n);
+  for (std::int64_t r = 0; r < n; ++r)
+    for (std::int64_t col = 0; col < n; ++col)
+      c.weights(r, col) = w[static_cast<std::size_t>(r * n + col)];
+  return c;
+}
+
+TrialRecord objective(const SparsityConfig& c, const ProxyBatch& batch, double penalty_weight,
+                      double sparsity_target, const DenseProxyCache* cache) {
+  c.validate();
+  if (!cache) {
+    const b200::ProxyCache pc(batch);
+    return pc.objective(c, penalty_weight, sparsity_target);
+  }
+  const std::vector<float> f = pack_features(batch);
+  const std::int64_t n = batch.grid.total_tokens;
+  if (cache->weights.rows() != n || cache->weights.cols() != n ||
+      static_cast<std::int64_t>(cache->row_sums.size()) != n)
+    throw std::invalid_argument("objective: cache does not match the batch");
+  std::vector<float> w(static_cast<std::size_t>(n * n));
+  for (std::int64_t r = 0; r < n; ++r)
+    for (std::int64_t col = 0; col < n; ++col)
+      w[static_cast<std::size_t>(r * n + col)] = cache->weights(r, col);
+  DeviceArray<float> dw(w.size()), df(f.size());
+  DeviceArray<double> drs(static_cast<std::size_t>(n));
+  dw.put(w.data(), w.size());
+  df.put(f.data(), f.size());
+  drs.put(cache->row_sums.data(), cache->row_sums.size());
+  const rp_grid gc = b200::to_c(batch.grid);
+  rp_proxy_cache* pc = nullptr;
+  check(rp_proxy_cache_from_weights(&gc, dw.get(), drs.get(), cache->reference_sq_norm, &pc,
+                                    nullptr));
+  try {
+    const TrialRecord r = run_objective(pc, c, batch.seed, df.get(), batch.feature_dim,
+                                        penalty_weight, sparsity_target);
+    rp_proxy_cache_destroy(pc);
+    return r;
+  } catch (...) {
+    rp_proxy_cache_destroy(pc);
+    throw;
+  }
+}
+
+namespace b200 {
+ProxyCache::ProxyCache(const ProxyBatch& batch)
+    : g_(batch.grid), seed_(batch.seed), dim_(batch.feature_dim) {
+  const std::vector<float> f = pack_features(batch);
+  cuda_ok(cudaMalloc(reinterpret_cast<void**>(&features_), f.size() * sizeof(float)));
+  cuda_ok(cudaMemcpy(features_, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice));
+  const rp_grid gc = to_c(g_);
+  const rp_status st = rp_proxy_cache_create(&gc, features_, dim_, &cache_, nullptr);
+  if (st != RP_OK) {
+    cudaFree(features_);
+    check(st);
+  }
+}
+
+ProxyCache::~ProxyCache() {
+  rp_proxy_cache_destroy(cache_);
+  if (features_) cudaFree(features_);
+}
+
+TrialRecord ProxyCache::objective(const SparsityConfig& c, double penalty_weight,
+                                  double sparsity_target) const {
+  c.validate();
+  return run_objective(cache_, c, seed_, features_, dim_, penalty_weight, sparsity_target);
+}
+}  // namespace b200
+
 }  // namespace radialplan

@@ -22,6 +22,7 @@
 
 #include "radialplan/attention.hpp"
 #include "radialplan/mask.hpp"
+#include "radialplan/profiler.hpp"
 #include "radialplan/radial.hpp"
 #include "radialplan/selection.hpp"
 
@@ -155,6 +156,36 @@ TEST_CASE("GPU operators or a loud failure") {
   CHECK(worst < 1e-5f);
 }
 
+// facade_selftest objective nf nt bs dim mode gamma lambda tm tc near far fk seed
+// prints loss mse sparsity (%.17g) without and with a host DenseProxyCache;
+// features f[t][d] = ((t*131 + d*71) % 97 - 48) / 32 (exact in any language).
+static int print_objective(int argc, char** argv) {
+  if (argc < 15) return 2;
+  ProxyBatch b;
+  b.grid = make_grid(std::atoi(argv[2]), std::atoi(argv[3]), std::atoi(argv[4]));
+  b.feature_dim = std::atoi(argv[5]);
+  b.seed = std::strtoull(argv[14], nullptr, 10);
+  b.features = Eigen::MatrixXf(b.grid.total_tokens, b.feature_dim);
+  for (std::int64_t t = 0; t < b.grid.total_tokens; ++t)
+    for (int d = 0; d < b.feature_dim; ++d)
+      b.features(t, d) = static_cast<float>((t * 131 + d * 71) % 97 - 48) / 32.0f;
+  SparsityConfig c;
+  c.mode = std::atoi(argv[6]) ? Mode::DynamicThreshold : Mode::StaticRatio;
+  c.radial.decay_factor = std::atof(argv[7]);
+  c.radial.long_range_factor = std::atof(argv[8]);
+  c.mask_threshold = std::atof(argv[9]);
+  c.col_threshold = std::atof(argv[10]);
+  c.near_param = std::atof(argv[11]);
+  c.far_param = std::atof(argv[12]);
+  c.fallback_k = std::atoi(argv[13]);
+  const TrialRecord a = objective(c, b, 10.0, 0.8);
+  const DenseProxyCache cache = build_proxy_cache(b);
+  const TrialRecord r = objective(c, b, 10.0, 0.8, &cache);
+  std::printf("%.17g %.17g %.17g\n%.17g %.17g %.17g\n%.17g\n", a.loss, a.mse,
+              a.achieved_sparsity, r.loss, r.mse, r.achieved_sparsity, cache.reference_sq_norm);
+  return 0;
+}
+
 static int print_mask(int argc, char** argv) {
   if (argc < 14) {
     std::fprintf(stderr, "usage: mask nf nt bs mode gamma lambda tm tc near far fk seed "
@@ -191,5 +222,6 @@ static int print_mask(int argc, char** argv) {
 
 int main(int argc, char** argv) {
   if (argc > 1 && std::strcmp(argv[1], "mask") == 0) return print_mask(argc, argv);
+  if (argc > 1 && std::strcmp(argv[1], "objective") == 0) return print_objective(argc, argv);
   return doctest::run_all();
 }

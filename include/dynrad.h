@@ -335,6 +335,13 @@ rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev,
                                 int feature_dim, rp_proxy_cache** out,
                                 rp_stream stream);
 
+/* The reference's DenseProxyCache itself (build_proxy_cache): weights
+ * [S, S] f32 row-major = exp(logit - row max), row_sums [S] f64 (device, may
+ * be NULL) and reference_sq_norm (host, may be NULL).  Synchronous. */
+rp_status rp_proxy_weights(const rp_grid* g, const float* features_dev, int feature_dim,
+                           float* weights_dev, double* row_sums_dev,
+                           double* reference_sq_norm, rp_stream stream);
+
 /* From a reference-layout DenseProxyCache already on the device: weights
  * [S, S] f32 row-major, row_sums [S] f64, and its reference_sq_norm. */
 rp_status rp_proxy_cache_from_weights(const rp_grid* g, const float* weights_dev,

@@ -283,6 +283,48 @@ std::vector<Eigen::MatrixXf> masked_attention_exact(const FeatureBatch& batch,
 std::vector<Eigen::MatrixXf> masked_attention(const FeatureBatch& batch, const TokenMask& mask,
                                               double epsilon = 1e-10);
 
+// ====================== profiler objective (profiler.hpp / proxy.hpp subset) ==
+// SURVEY 8f3.  Only the per-trial objective and its dense cache are on the
+// B200 path; the simulator, TPE search and LUT I/O stay out of scope.
+// proxy.hpp:26-33
+struct ProxyBatch {
+  GridSpec grid;
+  int feature_dim = 0;
+  double spatial_scale = 0.0;
+  double drift_rate = 0.0;
+  std::uint64_t seed = 0;
+  Eigen::MatrixXf features;  // total_tokens x feature_dim
+};
+
+// proxy.hpp:69: the features split into fused heads (q = k).
+FeatureBatch scoring_features(const ProxyBatch& batch, int fused_heads = 1);
+
+// profiler.hpp:43-49.
+struct TrialRecord {
+  int trial_index = 0;
+  SparsityConfig config;
+  double loss = 0.0;
+  double mse = 0.0;
+  double achieved_sparsity = 0.0;
+};
+
+// profiler.hpp:53-58.
+struct DenseProxyCache {
+  Eigen::MatrixXf weights;  // exp(logits - row max)
+  std::vector<double> row_sums;
+  double reference_sq_norm = 0.0;
+};
+
+// build_proxy_cache (profiler.cpp:49-78) on the GPU; returns the reference's
+// host layout (S x S weights).
+DenseProxyCache build_proxy_cache(const ProxyBatch& batch);
+
+// objective (profiler.hpp:68-76, profiler.cpp:80-148) on the GPU.  With a
+// cache, its weights are uploaded and reduced to block statistics; without,
+// the statistics are built on the device from the features.
+TrialRecord objective(const SparsityConfig& c, const ProxyBatch& batch, double penalty_weight,
+                      double sparsity_target, const DenseProxyCache* cache = nullptr);
+
 // ======================================= B200 device API (beyond the ref) ==
 namespace b200 {
 
@@ -341,6 +383,25 @@ void sparse_attention(const GridSpec& g, const DeviceTensor& q, const DeviceTens
                       const DeviceTensor& v, DeviceTensor& o, const std::int32_t* row_ptr,
                       const std::int32_t* col_idx, const std::int32_t* row_order,
                       float softmax_scale, rp_stream stream);
+
+// Device-resident proxy cache for a search loop: built once per batch
+// (block statistics, S x ceil(S/B) x 16 bytes), reused by every trial.
+class ProxyCache {
+ public:
+  explicit ProxyCache(const ProxyBatch& batch);
+  ~ProxyCache();
+  ProxyCache(const ProxyCache&) = delete;
+  ProxyCache& operator=(const ProxyCache&) = delete;
+  TrialRecord objective(const SparsityConfig& c, double penalty_weight,
+                        double sparsity_target) const;
+
+ private:
+  GridSpec g_;
+  std::uint64_t seed_ = 0;
+  int dim_ = 0;
+  float* features_ = nullptr;  // device [S, dim]
+  rp_proxy_cache* cache_ = nullptr;
+};
 
 }  // namespace b200
 }  // namespace radialplan

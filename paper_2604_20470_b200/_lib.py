@@ -162,6 +162,7 @@ _SIGS = {
     "rp_proxy_cache_create": ([_P(Grid), _v, C.c_int, _P(_v), _v], C.c_int),
     "rp_proxy_cache_from_weights": ([_P(Grid), _v, _v, C.c_double, _P(_v), _v], C.c_int),
     "rp_proxy_cache_destroy": ([_v], None),
+    "rp_proxy_weights": ([_P(Grid), _v, C.c_int, _v, _v, _P(C.c_double), _v], C.c_int),
     "rp_proxy_cache_stats": ([_v, _v, _P(C.c_double), _v], C.c_int),
     "rp_objective": ([_v, _P(Config), C.c_uint64, _v, C.c_int, C.c_double, C.c_double,
                       _P(Trial), _v, _v], C.c_int),

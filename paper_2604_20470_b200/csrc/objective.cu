@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads)
                     float scale, int block, int64_t unit, int64_t nbr,
                     const int* __restrict__ max_key, double* __restrict__ s1,
                     double* __restrict__ s2, float* __restrict__ diag,
-                    double* __restrict__ rs_part) {
+                    double* __restrict__ rs_part, float* __restrict__ w_out) {
   __shared__ __align__(16) float fr[kKC][kT + 4];
   __shared__ __align__(16) float fc[kKC][kT + 4];
   __shared__ float E[kT][kT + 1];
@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kThreads)
             rsum[i] += e;
             w = static_cast<float>(e);
             if (c == r) diag[r] = w;
+            if (w_out) w_out[r * n + c] = w;  // the reference's weights matrix
           }
           E[4 * ty + i][4 * tx + j] = w;
         }
@@ -391,9 +392,11 @@ using namespace rp::objective;
 
 extern "C" {
 
-rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev, int feature_dim,
-                                rp_proxy_cache** out, rp_stream stream) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace {
+void create_cache(const rp_grid* g, const float* features_dev, int feature_dim,
+                  rp_proxy_cache** out, float* weights_out, rp_stream stream) {
     require_device();
     check_grid(g);
     if (!out) throw std::invalid_argument("proxy cache: null output");
@@ -416,7 +419,7 @@ rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev, int
       RP_LAUNCHED();
       partials_kernel<false><<<grid, kThreads, 0, s>>>(
           features_dev, nullptr, n, feature_dim, scale, g->block_size, geo.unit, c->nbr, keys,
-          c->s1, c->s2, c->diag, rs_part);
+          c->s1, c->s2, c->diag, rs_part, weights_out);
       RP_LAUNCHED();
       finish_cache(c, rs_part, geo.splits, false, s);
       RP_CUDA(cudaFreeAsync(keys, s));
@@ -427,6 +430,37 @@ rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev, int
       throw;
     }
     *out = c;
+}
+}  // namespace
+
+extern "C" {
+
+rp_status rp_proxy_cache_create(const rp_grid* g, const float* features_dev, int feature_dim,
+                                rp_proxy_cache** out, rp_stream stream) {
+  return guarded([&] { create_cache(g, features_dev, feature_dim, out, nullptr, stream); });
+}
+
+rp_status rp_proxy_weights(const rp_grid* g, const float* features_dev, int feature_dim,
+                           float* weights_dev, double* row_sums_dev, double* reference_sq_norm,
+                           rp_stream stream) {
+  return guarded([&] {
+    if (!weights_dev) throw std::invalid_argument("proxy cache: null weights");
+    rp_proxy_cache* c = nullptr;
+    create_cache(g, features_dev, feature_dim, &c, weights_dev, stream);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const cudaError_t e1 =
+        row_sums_dev ? cudaMemcpyAsync(row_sums_dev, c->row_sums, sizeof(double) * c->n,
+                                       cudaMemcpyDeviceToDevice, s)
+                     : cudaSuccess;
+    const cudaError_t e2 = reference_sq_norm ? cudaMemcpyAsync(reference_sq_norm, c->sq,
+                                                               sizeof(double),
+                                                               cudaMemcpyDeviceToHost, s)
+                                             : cudaSuccess;
+    const cudaError_t e3 = cudaStreamSynchronize(s);
+    free_cache(c, s);
+    RP_CUDA(e1);
+    RP_CUDA(e2);
+    RP_CUDA(e3);
   });
 }
 
@@ -448,7 +482,7 @@ rp_status rp_proxy_cache_from_weights(const rp_grid* g, const float* weights_dev
       const dim3 grid(static_cast<unsigned>(geo.row_tiles), static_cast<unsigned>(geo.splits));
       partials_kernel<true><<<grid, kThreads, 0, s>>>(nullptr, weights_dev, c->n, 0, 0.f,
                                                       g->block_size, geo.unit, c->nbr, nullptr,
-                                                      c->s1, c->s2, c->diag, nullptr);
+                                                      c->s1, c->s2, c->diag, nullptr, nullptr);
       RP_LAUNCHED();
       // the caller's squared norm is kept as given (profiler.cpp:142 divides by it)
       RP_CUDA(cudaMemcpyAsync(c->sq, &reference_sq_norm, sizeof(double), cudaMemcpyHostToDevice, s));

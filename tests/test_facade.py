@@ -94,3 +94,35 @@ def test_facade_build_mask_vs_port(port, args):
                                     with_values=False)
     want = port.build_mask(nf, nt, bs, cfg, int(a[11]), q=q, k=k)
     assert np.array_equal(got, np.asarray(want, np.uint8).ravel())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [
+    # nf nt bs dim mode gamma lambda tm tc near far fk seed
+    "6 96 16 32 0 1.5 0.5 0.6 0.3 0.5 0.3 1 11",
+    "4 150 32 24 1 1.5 0.5 0.6 0.3 0.0 1.0 1 5",
+])
+def test_facade_objective_vs_port(port, args):
+    """radialplan::objective / build_proxy_cache on the facade (with and
+    without a host DenseProxyCache) against the restatement (bit-identical
+    to the reference's profiler.cpp, tests/test_oracle.py)."""
+    if not _have_gpu():
+        pytest.skip("no CUDA device")
+    from oracle import pyoracle
+    a = args.split()
+    r = _run(SELFTEST, "objective", *a)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.split("\n")
+    nf, nt, bs, dim, mode = (int(x) for x in a[:5])
+    t = np.arange(nf * nt)[:, None]
+    d = np.arange(dim)[None, :]
+    feats = (((t * 131 + d * 71) % 97 - 48) / 32.0).astype(np.float32)
+    gm, lm, tm, tc, near, far = (float(x) for x in a[5:11])
+    cfg = pyoracle.Cfg(mode, gm, lm, 1e-6, tm, tc, near, far, int(a[11]))
+    want = port.objective(nf, nt, bs, cfg, feats, int(a[12]), threads=4)
+    _, _, sq = port.proxy_cache(feats, threads=4)
+    for line in lines[:2]:
+        loss, mse, sp = (float(x) for x in line.split())
+        assert sp == want[2]
+        assert abs(mse - want[1]) <= 1e-9 * want[1] and abs(loss - want[0]) <= 1e-9 * want[0]
+    assert abs(float(lines[2]) - sq) <= 1e-12 * sq
