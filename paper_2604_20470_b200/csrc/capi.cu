@@ -21,6 +21,7 @@
 #include "umma_probe.cu"
 #include "attn_sm100_db.cu"
 #include "attn_sm100_rp.cu"
+#include "attn_sm100_rp2.cu"
 #include "csr.cu"
 
 namespace rp {
@@ -75,9 +76,12 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     // "rp" = block-row pairs of one head sharing every K/V tile
     // (attn_sm100_rp.cu: fastest on dense / long shared lists).  Measured side
     // by side in DESIGN.md section 8.
+    // "rp2" = row pairs sharing K/V with a double-buffered score tile per
+    // query tile at half-block granularity (attn_sm100_rp2.cu).
     static const int variant = [] {
       const char* e = std::getenv("DYNRAD_K6");
       if (e && std::strcmp(e, "rp") == 0) return 0;
+      if (e && std::strcmp(e, "rp2") == 0) return 2;
       return 1;
     }();
     // The kernels re-balance registers between warpgroups with setmaxnreg;
@@ -94,7 +98,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       done = true;
     };
-    if (variant == 0 && !soft_bits) {
+    if (variant != 1 && !soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
@@ -132,7 +136,19 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.out_head_stride = o.head_stride;
       p.scale_log2 = scale * 1.4426950408889634f;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-      if (d == 128) {
+      if (variant == 2) {
+        if (d == 128) {
+          static bool done = false;
+          const int smem = attn4::Layout<128>::kSmemBytes;
+          prepare(reinterpret_cast<const void*>(attn4::bsfa_fwd_rp2_kernel<128>), smem, done);
+          attn4::bsfa_fwd_rp2_kernel<128><<<grid, attn4::kThreads, smem, stream>>>(mq, mk, mv, p);
+        } else {
+          static bool done = false;
+          const int smem = attn4::Layout<64>::kSmemBytes;
+          prepare(reinterpret_cast<const void*>(attn4::bsfa_fwd_rp2_kernel<64>), smem, done);
+          attn4::bsfa_fwd_rp2_kernel<64><<<grid, attn4::kThreads, smem, stream>>>(mq, mk, mv, p);
+        }
+      } else if (d == 128) {
         static bool done = false;
         const int smem = attn3::Layout<128>::kSmemBytes;
         prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128>), smem, done);

@@ -589,6 +589,15 @@ def mask_to_csr(g: GridSpec, mask_dev, stream=None, out=None, trim: bool = True)
     return row_ptr, col_idx[:n], order
 
 
+def mask_to_bsr(g: GridSpec, mask_dev, stream=None):
+    """SURVEY 8f2 export: the block mask as a BSR matrix (indptr[S_b+1],
+    indices[nnz] int32, ascending per row, block R = C = g.block_size) -- the
+    layout FlashInfer's BlockSparseAttentionWrapper.plan and scipy.sparse.bsr
+    take (tools/flashinfer_compare.py runs FlashInfer on it)."""
+    row_ptr, col_idx, _ = mask_to_csr(g, mask_dev, stream=stream)
+    return row_ptr, col_idx
+
+
 def sparse_attention(g: GridSpec, q, k, v, row_ptr, col_idx, row_order=None, out=None,
                      softmax_scale: float = 0.0, stream=None):
     """Block-sparse attention forward on device tensors; out [S', heads, d]."""

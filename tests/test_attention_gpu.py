@@ -204,3 +204,17 @@ def test_host_pipeline_matches_device_path(cuda):
     row_ptr, col_idx, order = rp.mask_to_csr(g, torch.from_numpy(bits).cuda())
     dev = rp.sparse_attention(g, *(t.cuda() for t in x), row_ptr, col_idx, order).cpu()
     assert torch.equal(host, dev)
+
+
+def test_mask_to_bsr_matches_dense(cuda, port):
+    """BSR export (indptr / indices) of a reference mask."""
+    import scipy.sparse as sp
+    cfg = pyoracle.Cfg(0, 1.0, 0.3, 1e-6, 0.75, 0.2, 0.3, 0.3)
+    bits = port.build_mask(6, 500, 128, cfg, 7)
+    g = rp.make_grid(6, 500, 128)
+    indptr, indices = rp.mask_to_bsr(g, torch.from_numpy(np.ascontiguousarray(bits)).cuda())
+    nb = g.blocks_per_dim
+    dense = pyoracle.unpack_bits(bits, nb)
+    m = sp.csr_matrix((np.ones(indices.numel()), indices.cpu().numpy(), indptr.cpu().numpy()),
+                      shape=(nb, nb))
+    assert np.array_equal(m.toarray().astype(np.uint8), dense)
