@@ -502,7 +502,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            L.lib().rp_plan_destroy(h)
+            try:
+                L.lib().rp_plan_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     def build_mask_device(self, q=None, k=None, n_score_heads: int = 0, out=None,
