@@ -1,4 +1,5 @@
-// TEST INFRASTRUCTURE ONLY -- compile-only stand-in for nlohmann/json.
+// TEST INFRASTRUCTURE ONLY -- compile-only stand-in for nlohmann/json, used
+// by oracle/Makefile only when the cudnn_frontend copy of nlohmann is absent.
 //
 // The reference's profiler.cpp and proxy.cpp include <json.hpp> (nlohmann
 // json, a third-party dependency that is not vendored under /root/reference)
