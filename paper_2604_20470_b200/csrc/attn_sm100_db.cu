@@ -2,12 +2,12 @@
 // sm_100a, with the score tile double-buffered in TMEM.
 //
 // Replaces radialplan::masked_attention_exact (attention.cpp:50-121) on the
-// tensor cores, with the same semantics as attn_sm100.cu: only the row's CSR
+// tensor cores, with the reference's exact-mask semantics: only the row's CSR
 // blocks are attended (-inf elsewhere, constant per B x B block), and rows
 // >= S are TMA out-of-bounds zeros that take part as keys with logit 0
 // whenever their block is active (attention.cpp:43-48, 66-68).
 //
-// Why a second design.  In the two-head ping-pong kernel each head's score
+// Why this design.  In the first (since removed) two-head ping-pong kernel each head's score
 // tile S lives in one TMEM buffer that P overwrites, so S(j+1) can only be
 // computed after P(j).V(j) has read P(j): every KV step pays softmax latency
 // + MMA latency in series (measured: 2.1k + 1.4k clk per step, tensor pipe
@@ -23,7 +23,7 @@
 // P columns [32h, 32h+32) of the step's buffer, and O columns [hD/2, hD/2+D/2).
 // The row max is combined through shared memory with a 64-thread named
 // barrier per row group; the row sums stay per half until the epilogue.
-// Lazy rescaling (threshold 2^8, exact) as in attn_sm100.cu; a rescale waits
+// Lazy rescaling (threshold 2^8, exact: O and l are rebased together); a rescale waits
 // for the previous step's P.V to retire before touching O.
 //
 //   warps 0-7   softmax / epilogue       warp 8  TMA producer (whole warp)

@@ -1,7 +1,7 @@
 // K6 (v3): block-sparse flash-attention forward with two query row blocks of
 // the same head sharing every K/V tile (bf16 in / fp32 softmax, sm_100a).
 //
-// Same semantics as attn_sm100.cu / attn_sm100_db.cu (attention.cpp:50-121,
+// Same semantics as attn_sm100_db.cu (attention.cpp:50-121,
 // exact mask, zero-padded keys attended when their block is active).
 //
 // Why.  With one query tile per CTA every KV step streams a 32 KB K tile and
