@@ -244,10 +244,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DYNRAD_BENCH_SHARED_GPU=1 (validation only, never a reported number):
+    # every rank on cuda:0 over gloo, so the N > 1 code path (head shards,
+    # split scoring, broadcast / OR all-gather, max-over-ranks timing) can be
+    # exercised on a one-GPU box.
+    shared = os.environ.get("DYNRAD_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -270,11 +280,17 @@ def main():
     cfg = rp.SparsityConfig(rp.Mode(cfgd["mode"]), rp.RadialParams(gm, gl), tm, tc, a, b)
     S = g.total_tokens
     stream = torch.cuda.Stream(device=dev)
-    gen = torch.Generator(device=dev).manual_seed(42 + h0)
+    # The whole layer's Q/K/V from one seed on every rank, then this rank's
+    # head slice: every N sees the same data (and so the same dynamic mask).
+    gen = torch.Generator(device=dev).manual_seed(42)
     with torch.cuda.stream(stream):
-        q = torch.randn((S, Hl, d), device=dev, generator=gen).to(torch.bfloat16)
-        k = torch.randn((S, Hl, d), device=dev, generator=gen).to(torch.bfloat16)
-        v = torch.randn((S, Hl, d), device=dev, generator=gen).to(torch.bfloat16)
+        qkv = []
+        for _ in range(3):
+            full = torch.randn((S, H, d), device=dev, generator=gen).to(torch.bfloat16)
+            qkv.append(full[:, h0:h0 + Hl].contiguous())
+            del full
+        q, k, v = qkv
+        del qkv
         out = torch.empty((g.padded_tokens, Hl, d), device=dev, dtype=torch.bfloat16)
     stream.synchronize()
 
@@ -537,7 +553,7 @@ def main():
             "metric": METRIC, "value": ms, "unit": "ms/layer", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic N(0,1) Q/K/V (torch generator, seed 42)",
+            "dtype": "bf16", "data": "synthetic N(0,1) Q/K/V of the whole layer (torch generator, seed 42; each rank takes its head slice)",
             "config": {"workload": cfgd["workload"], "global_heads": H,
                        "seq_len": S, "padded_tokens": g.padded_tokens,
                        "block_size": cfgd["bs"], "mask_active_blocks": nnz,
