@@ -13,8 +13,11 @@
 //   pool      block means of the first H_f heads of Q and K over each block's
 //             valid tokens: one pass over 2 S H_f d bf16 -- HBM-bound,
 //             128-bit loads, fp32 accumulation, shared-memory reduction.
-//   select    one CTA per block row: s(r, c) = Qp_r . Kp_c / sqrt(d) / H_f over
-//             the candidates (warp dot products + shuffle reductions), a
+//   scores    s(r, c) = Qp_r . Kp_c / sqrt(d) / H_f for all block pairs as one
+//             tiled fp32 GEMM (64 x 64 tiles staged in shared memory, so each
+//             pooled key row is read from L2 once per 64 query rows instead of
+//             once per row: 1.7 GB -> 0.1 GB of L2 traffic at Hunyuan);
+//   select    one CTA per block row: the row's candidate scores, a
 //             bitonic sort (score descending, column ascending on ties), then
 //             static-ratio top-k (keep max(1, floor(ratio n)) best) or
 //             dynamic cumulative softmax mass (smallest prefix whose softmax
@@ -37,30 +40,33 @@ struct Dist {
   int32_t retained;  // frame pair at this distance survives the split rule
 };
 
-// 0 none, 1 candidate, 2 forced
-__global__ void classify_kernel(const Dist* __restrict__ tab, int nf, int64_t nt, int64_t S,
+// 0 none, 1 candidate, 2 forced (32-bit index arithmetic: S < 2^31)
+__global__ void classify_kernel(const Dist* __restrict__ tab, int nf, int64_t nt64, int64_t S64,
                                 int bs, int64_t nb, uint8_t* __restrict__ state) {
-  const int64_t r = blockIdx.y;
-  const int64_t t0 = r * bs, t1 = min(t0 + bs, S);  // valid query tokens [t0, t1)
-  for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nb;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t k0 = c * bs, k1 = min(k0 + bs, S);
+  const int nt = static_cast<int>(nt64), S = static_cast<int>(S64);
+  const int r = blockIdx.y;
+  const int t0 = r * bs, t1 = min(t0 + bs, S);  // valid query tokens [t0, t1)
+  const int fi0 = t0 / nt, fi1 = (t1 - 1) / nt;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nb; c += gridDim.x * blockDim.x) {
+    const int k0 = c * bs, k1 = min(k0 + bs, S);
     uint8_t st = 0;
     if (t0 < t1 && k0 < k1) {
-      for (int64_t fi = t0 / nt; fi <= (t1 - 1) / nt; ++fi) {
-        const int64_t ua = max(t0, fi * nt) - fi * nt, ub = min(t1 - 1, fi * nt + nt - 1) - fi * nt;
-        for (int64_t fj = k0 / nt; fj <= (k1 - 1) / nt; ++fj) {
-          const int64_t va = max(k0, fj * nt) - fj * nt, vb = min(k1 - 1, fj * nt + nt - 1) - fj * nt;
-          const int64_t t = fi > fj ? fi - fj : fj - fi;
+      const int fj0 = k0 / nt, fj1 = (k1 - 1) / nt;
+      for (int fi = fi0; fi <= fi1; ++fi) {
+        const int ua = max(t0, fi * nt) - fi * nt, ub = min(t1 - 1, fi * nt + nt - 1) - fi * nt;
+        for (int fj = fj0; fj <= fj1; ++fj) {
+          const int va = max(k0, fj * nt) - fj * nt, vb = min(k1 - 1, fj * nt + nt - 1) - fj * nt;
+          const int t = fi > fj ? fi - fj : fj - fi;
           if (t <= 1) {
             st = 2;
-          } else if (tab[t].retained && !(va - ub > tab[t].width || ua - vb > tab[t].width)) {
-            if (st == 0) st = 1;
+          } else {
+            const Dist dt = tab[t];
+            if (dt.retained && !(va - ub > dt.width || ua - vb > dt.width) && st == 0) st = 1;
           }
         }
       }
     }
-    state[r * nb + c] = st;
+    state[static_cast<int64_t>(r) * nb + c] = st;
   }
 }
 
@@ -104,56 +110,107 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   }
 }
 
-// One CTA (256 threads) per block row.  Dynamic shared memory: the row's
-// pooled query (F floats), then cap (score, column) pairs, cap a power of two
-// >= the block count.
-__global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ qp,
+// sc[r][c] = scale * Qp_r . Kp_c, 64 x 64 output tiles, 256 threads x 4 x 4
+// (measured against 128 x 128 / 8 x 8 and 32 x 32 / 64-thread tiles: the
+// middle size is fastest at both the Wan and the Hunyuan block counts).
+constexpr int kT = 64, kKC = 32, kST = 256;
+__global__ void __launch_bounds__(kST) scores_kernel(const float* __restrict__ qp,
                                                      const float* __restrict__ kp, int F,
-                                                     float scale, const uint8_t* __restrict__ state,
+                                                     int64_t nb, float scale,
+                                                     float* __restrict__ sc) {
+  __shared__ __align__(16) float fa[kKC][kT + 4];
+  __shared__ __align__(16) float fb[kKC][kT + 4];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kT, c0 = static_cast<int64_t>(blockIdx.x) * kT;
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < F; k0 += kKC) {
+    __syncthreads();
+    for (int idx = tid; idx < kT * kKC; idx += kST) {
+      const int row = idx / kKC, kk = idx % kKC;
+      const bool in = k0 + kk < F;
+      fa[kk][row] = in && r0 + row < nb ? qp[(r0 + row) * F + k0 + kk] : 0.f;
+      fb[kk][row] = in && c0 + row < nb ? kp[(c0 + row) * F + k0 + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kKC; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&fa[kk][4 * ty]);
+      const float4 b = *reinterpret_cast<const float4*>(&fb[kk][4 * tx]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + 4 * ty + i;
+    if (r >= nb) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = c0 + 4 * tx + j;
+      if (c < nb) sc[r * nb + c] = acc[i][j] * scale;
+    }
+  }
+}
+
+// One CTA (256 threads) per block row.  Dynamic shared memory: cap (score,
+// column) pairs (cap a power of two >= the block count) and one flag byte per
+// column.  Candidates are compacted with warp ballots + a block scan (no
+// shared-memory atomics: a single counter serialised ~1000 atomics per row),
+// the bitonic sort runs over the next power of two >= the candidate count,
+// and the row's words come from warp ballots (warp w of a pass owns 32
+// aligned columns).
+__global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ scores,
+                                                     const uint8_t* __restrict__ state,
                                                      int64_t nb, int64_t row_bytes, int cap,
                                                      int mode, double param,
                                                      uint8_t* __restrict__ bits) {
   extern __shared__ float sm[];
-  float* qrow = sm;                                   // [F]
-  float* sc = sm + F;                                 // [cap]
+  float* sc = sm;                                     // [cap]
   int* ci = reinterpret_cast<int*>(sc + cap);         // [cap]
-  uint32_t* words = reinterpret_cast<uint32_t*>(ci + cap);  // [row_bytes/4 + 1]
-  __shared__ int n_cand;
+  uint8_t* flag = reinterpret_cast<uint8_t*>(ci + cap);  // [cap]: 2 forced, 1 kept
+  __shared__ int wsum[8];
   __shared__ int n_keep;
   __shared__ double red_total;
   const int64_t r = blockIdx.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int f = threadIdx.x; f < F; f += blockDim.x) qrow[f] = qp[r * F + f];
-  const int nwords = static_cast<int>((row_bytes + 3) / 4);
-  for (int w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0u;
-  if (threadIdx.x == 0) n_cand = 0;
-  __syncthreads();
-  // candidate scores (warp per column), forced bits
-  for (int64_t c = warp; c < nb; c += blockDim.x / 32) {
-    const uint8_t st = state[r * nb + c];
-    if (st == 2 && lane == 0) atomicOr(&words[c / 32], 1u << (c % 32));
-    if (st != 1) continue;
-    float acc = 0.f;
-    for (int f = lane; f < F; f += 32) acc = fmaf(qrow[f], __ldg(kp + c * F + f), acc);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-    if (lane == 0) {
-      const int at = atomicAdd(&n_cand, 1);
-      sc[at] = acc * scale;
+  const float* srow = scores + r * nb;
+  const uint8_t* strow = state + r * nb;
+  // 1. compaction of the candidates in column order
+  int n = 0;
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    const int64_t c = base + threadIdx.x;
+    const uint8_t st = c < nb ? strow[c] : 0;
+    if (c < nb) flag[c] = st == 2 ? 2 : 0;
+    const bool cand = st == 1;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, cand);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = n;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    int tot = 0;
+    for (int w = 0; w < 8; ++w) tot += wsum[w];
+    if (cand) {
+      const int at = off + __popc(bal & ((1u << lane) - 1u));
+      sc[at] = srow[c];
       ci[at] = static_cast<int>(c);
     }
+    n += tot;
+    __syncthreads();
   }
-  __syncthreads();
-  const int n = n_cand;
-  for (int i = n + threadIdx.x; i < cap; i += blockDim.x) {
+  int cp = 1;
+  while (cp < n) cp <<= 1;
+  for (int i = n + threadIdx.x; i < cp; i += blockDim.x) {
     sc[i] = -INFINITY;
     ci[i] = 0x7FFFFFFF;
   }
   __syncthreads();
-  // bitonic sort: score descending, column ascending
-  for (int size = 2; size <= cap; size <<= 1) {
+  // 2. bitonic sort: score descending, column ascending
+  for (int size = 2; size <= cp; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < cap / 2; i += blockDim.x) {
+      for (int i = threadIdx.x; i < cp / 2; i += blockDim.x) {
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool desc = (lo & size) == 0;
@@ -170,6 +227,7 @@ __global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ q
       __syncthreads();
     }
   }
+  // 3. how many of the best to keep
   if (mode == RP_POOLED_TOPK) {
     if (threadIdx.x == 0) {
       int keep = n > 0 ? static_cast<int>(floor(static_cast<double>(n) * param)) : 0;
@@ -208,11 +266,16 @@ __global__ void __launch_bounds__(256) select_kernel(const float* __restrict__ q
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n_keep; i += blockDim.x) atomicOr(&words[ci[i] / 32], 1u << (ci[i] % 32));
+  for (int i = threadIdx.x; i < n_keep; i += blockDim.x) flag[ci[i]] = 1;
   __syncthreads();
+  // 4. the row's bits: one ballot per 32 aligned columns
   uint8_t* row = bits + r * row_bytes;
-  for (int64_t x = threadIdx.x; x < row_bytes; x += blockDim.x)
-    row[x] = static_cast<uint8_t>(words[x / 4] >> (8 * (x % 4)));
+  for (int64_t base = 32 * warp; base < 8 * row_bytes; base += blockDim.x) {
+    const int64_t c = base + lane;
+    const uint32_t w = __ballot_sync(0xFFFFFFFFu, c < nb && flag[c] != 0);
+    const int64_t byte0 = base / 8 + lane;  // lanes 0-3 store the word's bytes
+    if (lane < 4 && byte0 < row_bytes) row[byte0] = static_cast<uint8_t>(w >> (8 * lane));
+  }
 }
 
 }  // namespace pooled
@@ -245,12 +308,13 @@ rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor
     if (mode != RP_POOLED_TOPK && mode != RP_POOLED_MASS)
       throw std::invalid_argument("pooled select: unknown mode");
     if (!mask_bits_dev) throw std::invalid_argument("build_mask: null mask buffer");
+    if (g->padded_tokens >= (int64_t{1} << 31))
+      throw std::invalid_argument("pooled select: more than 2^31 tokens");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t nb = g->blocks_per_dim;
     int cap = 2;
     while (cap < nb) cap <<= 1;
-    const size_t smem = static_cast<size_t>(F) * 4 + static_cast<size_t>(cap) * 8 +
-                        static_cast<size_t>((g->row_bytes + 3) / 4 + 1) * 4;
+    const size_t smem = static_cast<size_t>(cap) * 9;
     if (smem > 200 * 1024) throw std::invalid_argument("pooled select: grid too large");
     // per-distance window and split decisions (radial.cpp:30-54)
     std::vector<pooled::Dist> tab(static_cast<size_t>(g->n_frames));
@@ -260,11 +324,12 @@ rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor
     }
     pooled::Dist* d_tab = nullptr;
     uint8_t* d_state = nullptr;
-    float *d_qp = nullptr, *d_kp = nullptr;
+    float *d_qp = nullptr, *d_kp = nullptr, *d_sc = nullptr;
     RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), sizeof(pooled::Dist) * tab.size(), s));
     RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_state), static_cast<size_t>(nb * nb), s));
     RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_qp), sizeof(float) * nb * F, s));
     RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_kp), sizeof(float) * nb * F, s));
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sc), sizeof(float) * nb * nb, s));
     RP_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(pooled::Dist) * tab.size(),
                             cudaMemcpyHostToDevice, s));
     pooled::classify_kernel<<<dim3(static_cast<unsigned>((nb + 255) / 256),
@@ -284,13 +349,18 @@ rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor
     }
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(q->head_dim)) /
                                            n_score_heads);
+    const unsigned tiles = static_cast<unsigned>((nb + pooled::kT - 1) / pooled::kT);
+    pooled::scores_kernel<<<dim3(tiles, tiles), pooled::kST, 0, s>>>(d_qp, d_kp, F, nb, scale,
+                                                                      d_sc);
+    RP_LAUNCHED();
     pooled::select_kernel<<<static_cast<unsigned>(nb), 256, smem, s>>>(
-        d_qp, d_kp, F, scale, d_state, nb, g->row_bytes, cap, mode, param, mask_bits_dev);
+        d_sc, d_state, nb, g->row_bytes, cap, mode, param, mask_bits_dev);
     RP_LAUNCHED();
     RP_CUDA(cudaFreeAsync(d_tab, s));
     RP_CUDA(cudaFreeAsync(d_state, s));
     RP_CUDA(cudaFreeAsync(d_qp, s));
     RP_CUDA(cudaFreeAsync(d_kp, s));
+    RP_CUDA(cudaFreeAsync(d_sc, s));
   });
 }
 
