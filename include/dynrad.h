@@ -288,6 +288,13 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g,
                                          int head_dim, void* o_host,
                                          rp_stream stream);
 
+/* Stage (b) of rp_pooled_select on its own: block means of the first n_heads
+ * heads of x (bf16 [tokens, heads, d]) -> out_dev [S_b, n_heads * d] f32.
+ * One pass over S * n_heads * d bf16 (HBM-bound; the bench's roofline for
+ * the pooled selector). */
+rp_status rp_block_mean_pool(const rp_grid* g, const rp_tensor* x, int n_heads,
+                             float* out_dev, rp_stream stream);
+
 /* ---------------------------------------------------- soft-mask attention --
  * masked_attention (attention.hpp:32-39, attention.cpp:59-81, 107-113): every
  * key takes part; logits get + log1p(epsilon) on active blocks and

@@ -175,6 +175,7 @@ _SIGS = {
     "rp_token_mask_to_blocks": ([_v, C.c_int64, C.c_int, _v, _P(C.c_int), _v], C.c_int),
     "rp_pooled_select": ([_P(Grid), _P(Config), _P(Tensor), _P(Tensor), C.c_int, C.c_int,
                           C.c_double, _v, _v], C.c_int),
+    "rp_block_mean_pool": ([_P(Grid), _P(Tensor), C.c_int, _v, _v], C.c_int),
     "rp_debug_umma_probe": ([_v, _v, _v, _v, _v, _v, _v], C.c_int),
 }
 

@@ -88,7 +88,25 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   for (int ch = threadIdx.x % 32; ch < chunks; ch += 32) {
     const int h = (ch * 8) / d, e = (ch * 8) % d;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int64_t t = t0 + grp; t < t1; t += 8) {
+    // four independent 16-byte loads in flight per thread (memory-level
+    // parallelism for the HBM stream); fp32 sums in token order per lane
+    int64_t t = t0 + grp;
+    for (; t + 24 < t1; t += 32) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = __ldg(reinterpret_cast<const uint4*>(x + (t + 8 * u) * ts + h * hs + e));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[2 * i] += __uint_as_float(w[i] << 16);
+          acc[2 * i + 1] += __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+      }
+    }
+    for (; t < t1; t += 8) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + t * ts + h * hs + e));
       const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -364,4 +382,29 @@ rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor
   });
 }
 
+rp_status rp_block_mean_pool(const rp_grid* g, const rp_tensor* x, int n_heads, float* out_dev,
+                             rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    check_grid(g);
+    if (!x || !x->data || x->dtype != RP_BF16)
+      throw std::invalid_argument("block mean pool: bf16 features required");
+    if (n_heads < 1 || n_heads > x->heads)
+      throw std::invalid_argument("block mean pool: n_heads out of range");
+    const int F = n_heads * x->head_dim;
+    if (F > pooled::kMaxFeat || x->head_dim % 8 || x->head_stride % 8 || x->token_stride % 8)
+      throw std::invalid_argument("pooled select: H_f * d <= 512, 16-byte aligned rows");
+    if (x->tokens < g->total_tokens)
+      throw std::invalid_argument("build_mask: feature batch too short");
+    if (!out_dev) throw std::invalid_argument("block mean pool: null output");
+    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(x->data);
+    pooled::pool_kernel<<<dim3(static_cast<unsigned>(g->blocks_per_dim), 1), 256, 0,
+                          reinterpret_cast<cudaStream_t>(stream)>>>(
+        p, p, x->token_stride, x->head_stride, n_heads, x->head_dim, g->total_tokens,
+        g->block_size, out_dev, out_dev);
+    RP_LAUNCHED();
+  });
+}
+
 }  // extern "C"
+

@@ -756,6 +756,20 @@ class ProxyCache:
             pass
 
 
+def block_mean_pool(g: GridSpec, x, n_heads: int, out=None, stream=None):
+    """Stage (b) of the pooled selector alone: block means of the first
+    n_heads heads of bf16 x [tokens, heads, d] -> float32 [S_b, n_heads * d]."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((g.blocks_per_dim, n_heads * x.shape[2]), dtype=torch.float32,
+                          device=x.device)
+    gc = g.c()
+    t = _tensor(x)
+    L.check(L.lib().rp_block_mean_pool(C.byref(gc), C.byref(t), n_heads,
+                                       C.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
+
+
 class PooledMode(enum.IntEnum):
     TopK = 0   # static ratio: keep max(1, floor(ratio * n)) best candidates per block row
     Mass = 1   # dynamic: smallest best-first prefix reaching a softmax mass

@@ -131,3 +131,16 @@ def test_pooled_selector_errors(cuda):
         rp.pooled_select(g, cfg, q, q, 1, rp.PooledMode.Mass, 1.5)
     with pytest.raises(rp.InvalidArgument):
         rp.pooled_select(g, cfg, q.float(), q.float(), 1, rp.PooledMode.TopK, 0.5)
+
+
+def test_block_mean_pool_stage_b(cuda):
+    """rp_block_mean_pool: block means of the first n heads, padded last block
+    averaged over its valid tokens only."""
+    g = rp.make_grid(3, 250, 128)
+    torch.manual_seed(0)
+    x = torch.randn(g.total_tokens, 4, 64, device="cuda").to(torch.bfloat16)
+    out = rp.block_mean_pool(g, x, 2).cpu().numpy()
+    xf = x[:, :2].reshape(g.total_tokens, 128).float().cpu().numpy().astype(np.float64)
+    B, S = g.block_size, g.total_tokens
+    want = np.stack([xf[b * B:min(S, b * B + B)].mean(0) for b in range(g.blocks_per_dim)])
+    assert np.abs(out - want).max() < 1e-5
