@@ -22,6 +22,7 @@
 #include "attn_sm100_db.cu"
 #include "attn_sm100_rp.cu"
 #include "attn_sm100_rp2.cu"
+#include "attn_sm100_alt.cu"
 #include "csr.cu"
 
 namespace rp {
@@ -82,6 +83,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       const char* e = std::getenv("DYNRAD_K6");
       if (e && std::strcmp(e, "rp") == 0) return 0;
       if (e && std::strcmp(e, "rp2") == 0) return 2;
+      if (e && std::strcmp(e, "alt") == 0) return 3;
       return 1;
     }();
     // The kernels re-balance registers between warpgroups with setmaxnreg;
@@ -98,7 +100,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       done = true;
     };
-    if (variant != 1 && !soft_bits) {
+    if ((variant == 0 || variant == 2) && !soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
@@ -164,6 +166,35 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
                         static_cast<void*>(pcol), static_cast<void*>(pflag),
                         static_cast<void*>(pord)})
         RP_CUDA(cudaFreeAsync(ptr, stream));
+      return;
+    }
+    if (variant == 3 && !soft_bits) {
+      // "alt": KV steps alternate between two softmax groups with separate
+      // accumulators (attn_sm100_alt.cu)
+      attn2::Params p{};
+      p.row_ptr = row_ptr;
+      p.col_idx = col_idx;
+      p.row_order = row_order;
+      p.n_rows = static_cast<int>(g.blocks_per_dim);
+      p.heads = q.heads;
+      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
+      p.out = static_cast<__nv_bfloat16*>(o.data);
+      p.out_tok_stride = o.token_stride;
+      p.out_head_stride = o.head_stride;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
+      if (d == 128) {
+        static bool done = false;
+        const int smem = attn5::Layout<128>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn5::bsfa_fwd_alt_kernel<128>), smem, done);
+        attn5::bsfa_fwd_alt_kernel<128><<<grid, attn5::kThreads, smem, stream>>>(mq, mk, mv, p);
+      } else {
+        static bool done = false;
+        const int smem = attn5::Layout<64>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn5::bsfa_fwd_alt_kernel<64>), smem, done);
+        attn5::bsfa_fwd_alt_kernel<64><<<grid, attn5::kThreads, smem, stream>>>(mq, mk, mv, p);
+      }
+      RP_LAUNCHED();
       return;
     }
     {
