@@ -433,6 +433,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 16; ++i) {
               if (c < 2) {
                 const int e = 32 * c + 2 * i;
+#ifdef RP_ABL_NOEXP
+                // ablation (timing only): no exponentials -- P = raw scores
+                pv_cur[i] = make_float2(S(e), S(e + 1));
+                (void)sc2;
+                (void)ng2;
+#else
                 if (track) lmax = fmaxf(lmax, fmaxf(S(e), S(e + 1)));
                 const float2 xv = ffma2v(make_float2(S(e), S(e + 1)), sc2, ng2);
                 if (kPolyMask & (1u << (i & 7))) {
@@ -441,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   pv_cur[i].x = ex2v(xv.x);
                   pv_cur[i].y = ex2v(xv.y);
                 }
+#endif
               }
               if (c > 0) {
                 acc[i & 1] = fadd2v(acc[i & 1], pv_prev[i]);
