@@ -23,6 +23,7 @@
 #include "attn_sm100_rp.cu"
 #include "attn_sm100_rp2.cu"
 #include "attn_sm100_alt.cu"
+#include "attn_sm100_2cta.cu"
 #include "csr.cu"
 
 namespace rp {
@@ -84,6 +85,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (e && std::strcmp(e, "rp") == 0) return 0;
       if (e && std::strcmp(e, "rp2") == 0) return 2;
       if (e && std::strcmp(e, "alt") == 0) return 3;
+      if (e && std::strcmp(e, "cta2") == 0) return 5;
       return 1;
     }();
     // The kernels re-balance registers between warpgroups with setmaxnreg;
@@ -100,7 +102,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       done = true;
     };
-    if ((variant == 0 || variant == 2) && !soft_bits) {
+    if ((variant == 0 || variant == 2 || variant == 5) && !soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
@@ -138,7 +140,17 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.out_head_stride = o.head_stride;
       p.scale_log2 = scale * 1.4426950408889634f;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-      if (variant == 2) {
+      if (variant == 5 && d == 128) {
+        // "cta2": CTA pairs with M = 256 tcgen05 MMAs (attn_sm100_2cta.cu)
+        static bool done = false;
+        const int smem = attn7::Layout::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn7::bsfa_fwd_2cta_kernel), smem, done);
+        const CUtensorMap mk64 = make_map_bf16(k, 64);
+        const int clusters =
+            static_cast<int>(std::min<long long>(p.n_units, std::max(1, sm_count() / 2)));
+        attn7::bsfa_fwd_2cta_kernel<<<2 * clusters, attn7::kThreads, smem, stream>>>(mq, mk64,
+                                                                                    mv, p);
+      } else if (variant == 2) {
         if (d == 128) {
           static bool done = false;
           const int smem = attn4::Layout<128>::kSmemBytes;

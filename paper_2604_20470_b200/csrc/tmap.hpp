@@ -29,15 +29,15 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D bf16 view {head_dim, heads, tokens} with a {64, 1, 128} box, 128B
+// 3-D bf16 view {head_dim, heads, tokens} with a {64, 1, box_rows} box, 128B
 // swizzle; rows >= tokens read as zero (the reference's zero padding).
-inline CUtensorMap make_map_bf16(const rp_tensor& t) {
+inline CUtensorMap make_map_bf16(const rp_tensor& t, unsigned box_rows = 128) {
   CUtensorMap m;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(t.head_dim), static_cast<cuuint64_t>(t.heads),
                         static_cast<cuuint64_t>(t.tokens)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(t.head_stride) * 2,
                            static_cast<cuuint64_t>(t.token_stride) * 2};
-  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t box[3] = {64, 1, box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, t.data, dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
