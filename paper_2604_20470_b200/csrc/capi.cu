@@ -54,6 +54,21 @@ static void check_tensor(const rp_tensor* t, const char* name) {
     throw std::invalid_argument(std::string("tensor ") + name + ": dtype must be f32 or bf16");
 }
 
+// Unit order of the stage-(d) kernels.  Natural (head-major, rows ascending):
+// the 148 concurrently running CTAs work on consecutive block rows of one
+// head, whose lists overlap, so K/V tiles are shared through L2.  LPT
+// (rows by descending list length, DYNRAD_ORDER=lpt) balances the tail but
+// scatters concurrent rows over the whole sequence: measured 8-9 % slower
+// at the Wan shape (56.5-57.4 % vs 61.9 % of peak).  The row_order argument
+// is therefore a hint that is used only under DYNRAD_ORDER=lpt.
+static bool use_lpt_order() {
+  static const bool lpt = [] {
+    const char* e = std::getenv("DYNRAD_ORDER");
+    return e && std::strcmp(e, "lpt") == 0;
+  }();
+  return lpt;
+}
+
 static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tensor& k,
                              const rp_tensor& v, rp_tensor& o, const int32_t* row_ptr,
                              const int32_t* col_idx, const int32_t* row_order, float scale,
@@ -62,6 +77,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
   // soft_bits != null: soft mask (masked_attention, attention.cpp:59-81) over
   // dense row lists; the block bit selects the log1p(eps) / log(eps) offset
   const int d = q.head_dim;
+  if (!use_lpt_order()) row_order = nullptr;
   const float user_scale = scale;
   if (scale <= 0.f) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
   if (q.dtype == RP_BF16) {
@@ -122,15 +138,17 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       attn3::pair_fill_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, prow,
                                                      pcol, pflag);
       RP_LAUNCHED();
-      csr::order_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, stream>>>(
-          pcnt, n_pairs, pord);
-      RP_LAUNCHED();
+      if (use_lpt_order()) {
+        csr::order_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, stream>>>(
+            pcnt, n_pairs, pord);
+        RP_LAUNCHED();
+      }
       attn3::Params p;
       p.row_ptr = row_ptr;
       p.prow_ptr = prow;
       p.pcol = pcol;
       p.pflag = pflag;
-      p.porder = pord;
+      p.porder = use_lpt_order() ? pord : nullptr;
       p.n_rows = n_rows;
       p.n_pairs = n_pairs;
       p.heads = q.heads;
