@@ -225,6 +225,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="wan_static", choices=sorted(CONFIGS))
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-rebuild", action="store_true",
+                    help="skip the warm static-mask rebuild measurement")
     ap.add_argument("--no-lib", action="store_true",
                     help="skip the FlashInfer block-sparse comparator (SURVEY 8f2)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -449,7 +451,7 @@ def main():
     # ---- static mask: warm rebuild (the one-time figure includes first-call
     # module loading and pool growth) ------------------------------------------
     static_warm = None
-    if not dynamic and rank == 0:
+    if not dynamic and rank == 0 and not args.no_rebuild:
         ts = []
         for _ in range(3):
             w0, w1 = ev(), ev()
