@@ -118,6 +118,27 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       done = true;
     };
+    // Per-row-unit parameters shared by db and alt (soft-mask fields zero
+    // unless soft_bits is set).
+    auto row_params = [&]() {
+      attn2::Params p{};
+      p.row_ptr = row_ptr;
+      p.col_idx = col_idx;
+      p.row_order = row_order;
+      p.n_rows = static_cast<int>(g.blocks_per_dim);
+      p.heads = q.heads;
+      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
+      p.out = static_cast<__nv_bfloat16*>(o.data);
+      p.out_tok_stride = o.token_stride;
+      p.out_head_stride = o.head_stride;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      p.soft_bits = soft_bits;
+      p.soft_row_bytes = g.row_bytes;
+      p.soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
+                                                    static_cast<double>(scale))
+                               : 0.f;
+      return p;
+    };
     if ((variant == 0 || variant == 2 || variant == 5) && !soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
@@ -201,17 +222,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     if (variant == 3 && !soft_bits) {
       // "alt": KV steps alternate between two softmax groups with separate
       // accumulators (attn_sm100_alt.cu)
-      attn2::Params p{};
-      p.row_ptr = row_ptr;
-      p.col_idx = col_idx;
-      p.row_order = row_order;
-      p.n_rows = static_cast<int>(g.blocks_per_dim);
-      p.heads = q.heads;
-      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
-      p.out = static_cast<__nv_bfloat16*>(o.data);
-      p.out_tok_stride = o.token_stride;
-      p.out_head_stride = o.head_stride;
-      p.scale_log2 = scale * 1.4426950408889634f;
+      const attn2::Params p = row_params();
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
       if (d == 128) {
         static bool done = false;
@@ -228,22 +239,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       return;
     }
     {
-      attn2::Params p;
-      p.row_ptr = row_ptr;
-      p.col_idx = col_idx;
-      p.row_order = row_order;
-      p.n_rows = static_cast<int>(g.blocks_per_dim);
-      p.heads = q.heads;
-      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
-      p.out = static_cast<__nv_bfloat16*>(o.data);
-      p.out_tok_stride = o.token_stride;
-      p.out_head_stride = o.head_stride;
-      p.scale_log2 = scale * 1.4426950408889634f;
-      p.soft_bits = soft_bits;
-      p.soft_row_bytes = g.row_bytes;
-      p.soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
-                                                    static_cast<double>(scale))
-                               : 0.f;
+      const attn2::Params p = row_params();
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
       if (d == 128) {
         static bool done = false;
