@@ -24,6 +24,7 @@
 #include "attn_sm100_rp2.cu"
 #include "attn_sm100_alt.cu"
 #include "attn_sm100_2cta.cu"
+#include "attn_sm100_mc.cu"
 #include "csr.cu"
 
 namespace rp {
@@ -102,6 +103,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (e && std::strcmp(e, "rp2") == 0) return 2;
       if (e && std::strcmp(e, "alt") == 0) return 3;
       if (e && std::strcmp(e, "cta2") == 0) return 5;
+      if (e && std::strcmp(e, "mc") == 0) return 6;
       return 1;
     }();
     // The kernels re-balance registers between warpgroups with setmaxnreg;
@@ -139,7 +141,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
                                : 0.f;
       return p;
     };
-    if ((variant == 0 || variant == 2 || variant == 5) && !soft_bits) {
+    if ((variant == 0 || variant == 2 || variant == 5 || variant == 6) && !soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
@@ -179,7 +181,17 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.out_head_stride = o.head_stride;
       p.scale_log2 = scale * 1.4426950408889634f;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-      if (variant == 5 && d == 128) {
+      if (variant == 6 && d == 128) {
+        // "mc": db per CTA, CTA pairs share their common K/V tiles by TMA
+        // multicast (attn_sm100_mc.cu)
+        static bool done = false;
+        const int smem = attn8::Layout<128>::kSmemBytes;
+        prepare(reinterpret_cast<const void*>(attn8::bsfa_fwd_mc_kernel<128>), smem, done);
+        const int clusters =
+            static_cast<int>(std::min<long long>(p.n_units, std::max(1, sm_count() / 2)));
+        attn8::bsfa_fwd_mc_kernel<128><<<2 * clusters, attn8::kThreads, smem, stream>>>(mq, mk,
+                                                                                     mv, p);
+      } else if (variant == 5 && d == 128) {
         // "cta2": CTA pairs with M = 256 tcgen05 MMAs (attn_sm100_2cta.cu)
         static bool done = false;
         const int smem = attn7::Layout::kSmemBytes;
