@@ -64,6 +64,13 @@ struct Params {
   long long out_tok_stride;
   long long out_head_stride;
   float scale_log2;
+  // Soft mask (masked_attention, attention.cpp:59-81; null = exact), as in
+  // attn_sm100_db.cu: own lists are dense and a block whose bit is clear
+  // gets the raw-logit offset soft_delta.
+  const int32_t* col_idx;   // own block lists (CSR, with row_ptr)
+  const uint8_t* soft_bits;
+  long long soft_row_bytes;
+  float soft_delta;
 };
 
 struct Unit {
@@ -138,7 +145,7 @@ __global__ void pair_fill_kernel(const int32_t* __restrict__ row_ptr,
   }
 }
 
-template <int D>
+template <int D, bool SOFT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     bsfa_fwd_rp_kernel(const __grid_constant__ CUtensorMap tq,
                        const __grid_constant__ CUtensorMap tk,
@@ -335,7 +342,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       float m = -INFINITY, l = 0.f;
+      const int my_beg = SOFT ? __ldg(p.row_ptr + my_row) : 0;
       for (int j = 0; j < my_cnt; ++j) {
+        float dlt = 0.f;  // soft-mask offset of this block (0: exact mode / active)
+        if constexpr (SOFT) {
+          const int c = __ldg(p.col_idx + my_beg + j);
+          const uint8_t by = __ldg(p.soft_bits + my_row * p.soft_row_bytes + (c >> 3));
+          dlt = ((by >> (c & 7)) & 1) ? 0.f : p.soft_delta;
+        }
         mbar_wait(&s_full[x], scnt & 1);
         ++scnt;
         tc_fence_after();
@@ -353,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float a = S(0);
 #pragma unroll
           for (int i = 1; i < 127; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
-          m = fmaxf(a, S(127));
+          m = fmaxf(a, S(127)) + dlt;
         }
         // exponentials against the (stale) reference max, 32-key chunks:
         // a chunk's exponentials overlap the packing and TMEM store of the
@@ -362,7 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float lmax = -INFINITY;
         auto exps = [&](float mref, bool track) {
           const float2 sc2 = make_float2(sl2, sl2);
-          const float2 ng2 = make_float2(-mref * sl2, -mref * sl2);
+          const float nb = (dlt - mref) * sl2;
+          const float2 ng2 = make_float2(nb, nb);
           acc[0] = acc[1] = make_float2(0.f, 0.f);
           float2 pv_prev[8];
 #pragma unroll
@@ -394,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         exps(m, j > 0);
         if (j > 0) {
+          lmax += dlt;
           const bool need = (lmax - m) * sl2 > 8.0f;
           if (__any_sync(0xFFFFFFFFu, need)) {
             // rebase on the new max: O_x is stable here (S_x(j) was issued

@@ -141,7 +141,9 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
                                : 0.f;
       return p;
     };
-    if ((variant == 0 || variant == 2 || variant == 5 || variant == 6) && !soft_bits) {
+    // the soft mask's dense lists run on the row-pair kernel (rp: fastest on
+    // dense masks)
+    if (variant == 0 || variant == 2 || variant == 5 || variant == 6 || soft_bits) {
       // union block lists of the row pairs (2p, 2p+1), LPT order
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
@@ -180,8 +182,14 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.out_tok_stride = o.token_stride;
       p.out_head_stride = o.head_stride;
       p.scale_log2 = scale * 1.4426950408889634f;
+      p.col_idx = col_idx;
+      p.soft_bits = soft_bits;
+      p.soft_row_bytes = g.row_bytes;
+      p.soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
+                                                    static_cast<double>(scale))
+                               : 0.f;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-      if (variant == 6 && d == 128) {
+      if (variant == 6 && d == 128 && !soft_bits) {
         // "mc": db per CTA, CTA pairs share their common K/V tiles by TMA
         // multicast (attn_sm100_mc.cu)
         static bool done = false;
@@ -191,7 +199,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
             static_cast<int>(std::min<long long>(p.n_units, std::max(1, sm_count() / 2)));
         attn8::bsfa_fwd_mc_kernel<128><<<2 * clusters, attn8::kThreads, smem, stream>>>(mq, mk,
                                                                                      mv, p);
-      } else if (variant == 5 && d == 128) {
+      } else if (variant == 5 && d == 128 && !soft_bits) {
         // "cta2": CTA pairs with M = 256 tcgen05 MMAs (attn_sm100_2cta.cu)
         static bool done = false;
         const int smem = attn7::Layout::kSmemBytes;
@@ -201,7 +209,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
             static_cast<int>(std::min<long long>(p.n_units, std::max(1, sm_count() / 2)));
         attn7::bsfa_fwd_2cta_kernel<<<2 * clusters, attn7::kThreads, smem, stream>>>(mq, mk64,
                                                                                     mv, p);
-      } else if (variant == 2) {
+      } else if (variant == 2 && !soft_bits) {
         if (d == 128) {
           static bool done = false;
           const int smem = attn4::Layout<128>::kSmemBytes;
@@ -212,6 +220,20 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
           const int smem = attn4::Layout<64>::kSmemBytes;
           prepare(reinterpret_cast<const void*>(attn4::bsfa_fwd_rp2_kernel<64>), smem, done);
           attn4::bsfa_fwd_rp2_kernel<64><<<grid, attn4::kThreads, smem, stream>>>(mq, mk, mv, p);
+        }
+      } else if (soft_bits) {
+        if (d == 128) {
+          static bool done = false;
+          const int smem = attn3::Layout<128>::kSmemBytes;
+          prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128, true>), smem, done);
+          attn3::bsfa_fwd_rp_kernel<128, true><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv,
+                                                                                       p);
+        } else {
+          static bool done = false;
+          const int smem = attn3::Layout<64>::kSmemBytes;
+          prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<64, true>), smem, done);
+          attn3::bsfa_fwd_rp_kernel<64, true><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv,
+                                                                                      p);
         }
       } else if (d == 128) {
         static bool done = false;
