@@ -54,7 +54,7 @@ struct Layout {
 #endif
   static constexpr int kSmemData = 2 * kTileBytes + kStages * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 13 + 2;
-  static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128) * 4;  // row max x2 slots, row sums
+  static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128 + 2 * 2 * 128) * 4;  // max, sums, block sums
   static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + kRedBytes + 1024;
   static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory");
   static constexpr uint32_t kO = 256;  // TMEM column of O
@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
   float* red_max = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 halves][128]
   float* red_l = red_max + 2 * 2 * 128;                       // [2 halves][128]
+  float* red_sum = red_l + 2 * 128;                           // [2 slots][2 halves][128]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -406,6 +407,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
           return fmaxf(slot[r], slot[128 + r]);
         };
+        // the two halves' sums of this block's exponentials (own slots: the
+        // slow path below may exchange a max in the same step)
+        auto exchange_sum = [&](float mine) -> float {
+          float* slot = red_sum + b * 256;
+          slot[half * 128 + r] = mine;
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+          return slot[r] + slot[128 + r];
+        };
         if (j == 0) {  // first block of the unit: the reference max comes first
           float a = S(0);
 #pragma unroll
@@ -458,11 +467,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
           }
         };
-        exps(m, j > 0);
-        if (j > 0) {
-          // this block's max (both halves): if it overtook the reference by
-          // more than 2^8, rebase O and l on the new max and redo the block
-          // (rare after the first blocks; exact either way)
+        exps(m, false);
+        // Rescale guard without a per-element max: if this block's
+        // exponentials (against the stale reference m) sum to <= 2^8 over the
+        // row, every one of them is <= 2^8, i.e. the block's max is within
+        // 2^8 of m and no rescale is due.  Only otherwise (rare after the
+        // first blocks) is the block max computed and exchanged, and O / l
+        // rebased when it overtook m by more than 2^8 (exact either way).
+        // Both halves see the same row sum, so they take the same branch.
+        const float2 at0 = fadd2(acc[0], acc[1]);
+        const float tot = j > 0 ? exchange_sum(at0.x + at0.y) : 0.f;
+        if (j > 0 && __any_sync(0xFFFFFFFFu, !(tot <= 256.0f))) {
+          float a = S(0);
+#pragma unroll
+          for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
+          lmax = fmaxf(a, S(63));
           const float mx = exchange_max(lmax + dlt);
           const bool need = (mx - m) * sl2 > 8.0f;
           if (__any_sync(0xFFFFFFFFu, need)) {
