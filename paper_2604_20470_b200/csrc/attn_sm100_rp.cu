@@ -407,9 +407,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 8; ++i) pv_prev[i] = pv_cur[i];
           }
         };
-        exps(m, j > 0);
-        if (j > 0) {
-          lmax += dlt;
+        exps(m, false);
+        // rescale guard from the row sum (see attn_sm100_db.cu): a block
+        // whose exponentials sum to <= 2^8 cannot hold a max more than 2^8
+        // above the reference; only otherwise is the block max computed
+        const float2 at0 = fadd2(acc[0], acc[1]);
+        if (j > 0 && __any_sync(0xFFFFFFFFu, !(at0.x + at0.y <= 256.0f))) {
+          float a = S(0);
+#pragma unroll
+          for (int i = 1; i < 127; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
+          lmax = fmaxf(a, S(127)) + dlt;
           const bool need = (lmax - m) * sl2 > 8.0f;
           if (__any_sync(0xFFFFFFFFu, need)) {
             // rebase on the new max: O_x is stable here (S_x(j) was issued
