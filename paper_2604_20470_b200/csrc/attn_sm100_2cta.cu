@@ -51,7 +51,7 @@ struct Layout {
   static constexpr int kStages = 8;
   static constexpr int kSmemData = 2 * kTileBytes + kStages * kHalfBytes;
   static constexpr int kNumBars = 2 * kStages + 16;
-  static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128) * 4;
+  static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128 + 2 * 2 * 128) * 4;
   static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + kRedBytes + 1024;
   static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory");
   static constexpr uint32_t kO = 256;
@@ -195,6 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
   float* red_max = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 halves][128]
   float* red_l = red_max + 2 * 2 * 128;                       // [2 halves][128]
+  float* red_sum = red_l + 2 * 128;                           // [2 slots][2 halves][128]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -456,8 +457,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
             }
           };
-          exps(m, !first);
+          exps(m, false);
+          // rescale guard from the exchanged row sum (see attn_sm100_db.cu)
+          const float2 at0 = fadd2(acc[0], acc[1]);
+          float tot = 0.f;
           if (!first) {
+            float* slot = red_sum + b * 256;
+            slot[half * 128 + r] = at0.x + at0.y;
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+            tot = slot[r] + slot[128 + r];
+          }
+          if (!first && __any_sync(0xFFFFFFFFu, !(tot <= 256.0f))) {
+            float a = S(0);
+#pragma unroll
+            for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
+            lmax = fmaxf(a, S(63));
             const float mx = exchange_max(lmax);
             const bool need = (mx - m) * sl2 > 8.0f;
             if (__any_sync(0xFFFFFFFFu, need)) {
