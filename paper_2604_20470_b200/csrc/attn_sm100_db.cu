@@ -54,7 +54,10 @@ struct Layout {
 #endif
   static constexpr int kSmemData = 2 * kTileBytes + kStages * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 13 + 2;
-  static constexpr int kRedBytes = (2 * 2 * 128 + 2 * 128 + 2 * 2 * 128) * 4;  // max, sums, block sums
+  // row max x2 slots, row sums, block sums x2 slots, lagged block sums x4
+  // slots, per-row |Q|^2 halves x2 Q buffers
+  static constexpr int kRedBytes =
+      (2 * 2 * 128 + 2 * 128 + 2 * 2 * 128 + 4 * 2 * 128 + 2 * 2 * 128) * 4;
   static constexpr int kSmemBytes = kSmemData + kNumBars * 8 + 16 + kRedBytes + 1024;
   static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory");
   static constexpr uint32_t kO = 256;  // TMEM column of O
@@ -76,6 +79,10 @@ struct Params {
   long long out_tok_stride;
   long long out_head_stride;
   float scale_log2;
+  // Per-head max_t |k_t| (may be null): enables the exchange-free rescale
+  // protocol for units whose logits provably stay within 2^64 of the first
+  // block's max (see the softmax below).
+  const float* kmax_head;
   // Soft mask (masked_attention, attention.cpp:59-81; null = exact mask):
   // the row lists are dense and a block whose bit is clear gets the logit
   // offset soft_delta = (log eps - log1p eps) / scale (raw-logit units; the
@@ -142,6 +149,29 @@ struct Cursor {
   RP_DEV int col(const Params& p) const { return shfl0(__ldg(p.col_idx + beg + j)); }
 };
 
+// max_t |k_t| per head (the logit bound of the exchange-free rescale
+// protocol): one thread per (token, head), 16-byte loads, fp32 sum of squares,
+// atomicMax on the non-negative float's bits.
+__global__ void kmax_kernel(const __nv_bfloat16* __restrict__ k, long long tokens, int heads,
+                            int d, long long ts, long long hs, float* __restrict__ kmax) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= tokens * heads) return;
+  const long long t = i / heads;
+  const int h = static_cast<int>(i % heads);
+  const uint4* row = reinterpret_cast<const uint4*>(k + t * ts + h * hs);
+  float acc = 0.f;
+  for (int c = 0; c < d / 8; ++c) {
+    const uint4 u = __ldg(row + c);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
+      acc = fmaf(lo, lo, fmaf(hi, hi, acc));
+    }
+  }
+  atomicMax(reinterpret_cast<int*>(kmax + h), __float_as_int(sqrtf(acc)));
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     bsfa_fwd_db_kernel(const __grid_constant__ CUtensorMap tq,
@@ -168,6 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* red_max = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 halves][128]
   float* red_l = red_max + 2 * 2 * 128;                       // [2 halves][128]
   float* red_sum = red_l + 2 * 128;                           // [2 slots][2 halves][128]
+  float* red_lag = red_sum + 2 * 2 * 128;                     // [4 slots][2 halves][128]
+  float* red_qn = red_lag + 4 * 2 * 128;                      // [2 Q buffers][2 halves][128]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -343,6 +375,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         tmem_st16(trow + L::qt_col(qb) + half * 16, v);
       }
+      if (p.kmax_head) {  // this half's |q_row|^2 for the unit's logit bound
+        float qq = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kUnits * 2; ++t) {
+          const float lo = __uint_as_float(v[t] << 16), hi = __uint_as_float(v[t] & 0xFFFF0000u);
+          qq = fmaf(lo, lo, fmaf(hi, hi, qq));
+        }
+        red_qn[(qb * 2 + half) * 128 + r] = qq;
+      }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -379,6 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float m = -INFINITY;  // running max (raw logits), possibly stale
       float l = 0.f;        // this half's row sum
+      // exchange-free mode for this unit (decided at j == 0, identically in
+      // both halves): own block sums of the last two steps, the step of the
+      // last rebase
+      bool lag = false;
+      float own1 = 0.f, own2 = 0.f;
+      int last_rebase = 0;
       for (int j = 0; j < n; ++j, ++g) {
         const uint32_t b = g & 1;
         const uint32_t sb = b * 128;
@@ -420,6 +467,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
           m = exchange_max(fmaxf(a, S(63)) + dlt);
+          if (p.kmax_head) {
+            // s = q.k <= |q||k| <= |q| max_t |k_t|: if that bound is within
+            // 2^64 of the first block's max (the reference m only grows),
+            // no exponential of this unit can overflow, and rescaling may
+            // be decided two steps late from the halves' block sums, which
+            // needs no per-step exchange.  Inputs are the same in both
+            // halves (m exchanged, |q|^2 halves in shared memory), so both
+            // take the same decision.
+            const int qb = ord & 1;
+            const float qq = red_qn[(qb * 2) * 128 + r] + red_qn[(qb * 2 + 1) * 128 + r];
+            const float bound = sqrtf(qq) * __ldg(p.kmax_head + h) * 1.001f + 1e-3f;
+            lag = __all_sync(0xFFFFFFFFu, (bound - m) * sl2 < 64.0f);
+          }
         }
         // p = 2^((s - m) * scale * log2 e) against the running reference m
         // (stale: the max of the previous blocks, so the exponentials do not
@@ -467,6 +527,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 16; ++i) pv_prev[i] = pv_cur[i];
           }
         };
+        // O must hold P(g-1).V(g-1) before a rescale
+        auto rescale_o = [&](float alpha) {
+          mbar_wait(pv_done, (g - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) {
+            uint32_t o[32];
+            const uint32_t oc = trow + L::kO + half * (D / 2) + c * 32;
+            tmem_ld32(oc, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(oc, o);
+          }
+        };
+        if (lag) {
+          // Lagged rebase: step j-2's block sums (own + partner's, both
+          // written before their P(g-2) arrive; S(g) was issued after P(g-2).V,
+          // so that barrier phase is complete and this wait acquires them)
+          // bound that block's exponentials; if the row's exceeded 2^8,
+          // rebase O, l and m by it before this step's exponentials.  Sums
+          // from before the last rebase are stale and skipped.
+          if (j >= 2 && j - 2 >= last_rebase) {
+            mbar_wait(&p_full[(g - 2) & 1], ((g - 2) >> 1) & 1);
+            const float T = own2 + red_lag[(((g - 2) & 3) * 2 + (half ^ 1)) * 128 + r];
+            const bool need = !(T <= 256.0f);
+            if (__any_sync(0xFFFFFFFFu, need)) {
+              const float lt = need ? __log2f(T) : 0.f;
+              const float alpha = need ? ex2(-lt) : 1.0f;
+              if (need) {
+                m += lt / sl2;
+                l *= alpha;
+              }
+              rescale_o(alpha);
+              last_rebase = j;
+            }
+          }
+          exps(m, false);
+          const float2 at0 = fadd2(acc[0], acc[1]);
+          own2 = own1;
+          own1 = at0.x + at0.y;
+          red_lag[((g & 3) * 2 + half) * 128 + r] = own1;
+        } else {
         exps(m, false);
         // Rescale guard without a per-element max: if this block's
         // exponentials (against the stale reference m) sum to <= 2^8 over the
@@ -490,21 +593,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               m = mx;
               l *= alpha;
             }
-            // O must hold P(g-1).V(g-1) before it is rescaled
-            mbar_wait(pv_done, (g - 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < D / 64; ++c) {
-              uint32_t o[32];
-              const uint32_t oc = trow + L::kO + half * (D / 2) + c * 32;
-              tmem_ld32(oc, o);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st32(oc, o);
-            }
+            rescale_o(alpha);
             exps(m, false);
           }
+        }
         }
         if (tr) RP_TR2(11, g);
         const float2 at = fadd2(acc[0], acc[1]);

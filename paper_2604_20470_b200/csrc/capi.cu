@@ -273,7 +273,24 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       return;
     }
     {
-      const attn2::Params p = row_params();
+      attn2::Params p = row_params();
+      // per-head max |k| for the exchange-free rescale protocol (one read of
+      // K, ~1 % of the layer); DYNRAD_DB_LAG=0 turns it off
+      static const bool lag_on = [] {
+        const char* e = std::getenv("DYNRAD_DB_LAG");
+        return !(e && std::strcmp(e, "0") == 0);
+      }();
+      float* kmax = nullptr;
+      if (lag_on && k.head_dim % 8 == 0) {
+        RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kmax), sizeof(float) * k.heads, stream));
+        RP_CUDA(cudaMemsetAsync(kmax, 0, sizeof(float) * k.heads, stream));
+        const long long n = k.tokens * k.heads;
+        attn2::kmax_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(k.data), k.tokens, k.heads, k.head_dim,
+            k.token_stride, k.head_stride, kmax);
+        RP_LAUNCHED();
+        p.kmax_head = kmax;
+      }
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
       if (d == 128) {
         static bool done = false;
@@ -287,6 +304,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
         attn2::bsfa_fwd_db_kernel<64><<<grid, attn2::kThreads, smem, stream>>>(mq, mk, mv, p);
       }
       RP_LAUNCHED();
+      if (kmax) RP_CUDA(cudaFreeAsync(kmax, stream));
       return;
     }
   } else {

@@ -218,3 +218,28 @@ def test_mask_to_bsr_matches_dense(cuda, port):
     m = sp.csr_matrix((np.ones(indices.numel()), indices.cpu().numpy(), indptr.cpu().numpy()),
                       shape=(nb, nb))
     assert np.array_equal(m.toarray().astype(np.uint8), dense)
+
+
+@pytest.mark.parametrize("kscale", [1.0, 4.0, 40.0])
+def test_bf16_rescale_paths_vs_torch(cuda, kscale):
+    """Logits that grow along the key axis (K scaled by a ramp) force the
+    online softmax to rebase: kscale 1-4 runs the exchange-free lagged rescale
+    (the |q| max|k| bound stays within 2^64 of the first block's max), 40 makes
+    that bound too loose so units fall back to the per-step exchange."""
+    nf, nt, bs, H, d = 4, 512, 128, 2, 128
+    S = nf * nt
+    g = rp.make_grid(nf, nt, bs)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn(S, H, d, device="cuda", generator=gen)
+    ramp = torch.linspace(0.2, 1.0, S, device="cuda")[:, None, None] * kscale
+    k = torch.randn(S, H, d, device="cuda", generator=gen) * ramp
+    v = torch.randn(S, H, d, device="cuda", generator=gen)
+    q, k, v = (x.to(torch.bfloat16) for x in (q, k, v))
+    nb = g.blocks_per_dim
+    dense = _random_mask(nb, 0.6, 3)
+    mdev = torch.from_numpy(pyoracle.pack_dense(dense)).cuda()
+    rpt, col, order = rp.mask_to_csr(g, mdev)
+    out = rp.sparse_attention(g, q, k, v, rpt, col, order)
+    ref = _torch_ref(q, k, v, dense, bs, S)
+    err = rel_rows(out[:S].float().cpu().numpy(), ref[:S].cpu().numpy())
+    assert err < 2e-2, err
