@@ -274,11 +274,15 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     }
     {
       attn2::Params p = row_params();
-      // per-head max |k| for the exchange-free rescale protocol (one read of
-      // K, ~1 % of the layer); DYNRAD_DB_LAG=0 turns it off
+      // Exchange-free rescale protocol (DYNRAD_DB_LAG=1; off by default): a
+      // per-head max |k| pre-pass (one read of K) lets units skip the
+      // per-step exchange.  Single launches gain ~3.5 points, but under
+      // sustained back-to-back load (bench.py, tools/ab_k6.py: mean of 20)
+      // it measured ~2 % slower (the pre-pass plus the power-capped clock),
+      // so the default keeps the exchange.
       static const bool lag_on = [] {
         const char* e = std::getenv("DYNRAD_DB_LAG");
-        return !(e && std::strcmp(e, "0") == 0);
+        return e && std::strcmp(e, "1") == 0;
       }();
       float* kmax = nullptr;
       if (lag_on && k.head_dim % 8 == 0) {
