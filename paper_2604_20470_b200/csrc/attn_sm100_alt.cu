@@ -37,7 +37,7 @@ constexpr int kThreads = 384;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
 #ifndef RP_ALT_POLY_MASK
-#define RP_ALT_POLY_MASK 0x01u
+#define RP_ALT_POLY_MASK 0x00u
 #endif
 constexpr uint32_t kPolyMask = RP_ALT_POLY_MASK;
 

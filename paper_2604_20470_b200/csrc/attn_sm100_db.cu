@@ -36,9 +36,12 @@ namespace attn2 {
 constexpr int kThreads = 384;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
-// Pairs (of every 8) whose exp2 runs as a polynomial on the FMA pipe.
+// Pairs (of every 8) whose exp2 runs as a polynomial on the FMA pipe.  None
+// by default: single launches are ~equal at 0 or 1 of 8, but under sustained
+// (power-capped) load the extra FMA-pipe instructions cost more than the MUFU
+// relief (tools/ab_k6.py: 22.86 vs 23.05 ms; 2 of 8: 23.46 ms).
 #ifndef RP_DB_POLY_MASK
-#define RP_DB_POLY_MASK 0x01u
+#define RP_DB_POLY_MASK 0x00u
 #endif
 constexpr uint32_t kPolyMask = RP_DB_POLY_MASK;
 
