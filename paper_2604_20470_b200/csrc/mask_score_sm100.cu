@@ -341,9 +341,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t k1 = 0u, u1 = 0u;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float x = __uint_as_float(sv[w4][i]);
-            k1 |= (x >= hi_raw ? 1u : 0u) << i;
-            u1 |= (x > lo_raw ? 1u : 0u) << i;
+            // compare + predicated OR per mask (2 instructions per bit)
+            asm("{\n\t.reg .pred pk, pu;\n\t"
+                "setp.ge.f32 pk, %2, %3;\n\t"
+                "setp.gt.f32 pu, %2, %4;\n\t"
+                "@pk or.b32 %0, %0, %5;\n\t"
+                "@pu or.b32 %1, %1, %5;\n\t}"
+                : "+r"(k1), "+r"(u1)
+                : "f"(__uint_as_float(sv[w4][i])), "f"(hi_raw), "f"(lo_raw), "r"(1u << i));
           }
           kb[w4] = k1 & inm[w4];
           ub[w4] = u1 & inm[w4] & ~k1;
