@@ -27,9 +27,11 @@
 // (it can only change a tile when fallback_k >= ceil(theta_c * B)).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -56,6 +58,8 @@ struct SParams {
   const DJob* jobs;
   const ScoreItem* items;
   long long n_items;
+  const int2* units;  // [n_units] item ranges [x, y), see UnitCursor
+  int n_units;
   int nt, bs, cph;       // tokens per frame, block size, 64-wide chunks per head
   float score_scale;     // inv_sqrt_d / H_f
   double* item_stats;    // pass 1: [n_items][3] (n, mean, M2)
@@ -63,8 +67,8 @@ struct SParams {
   const float2* job_thr;     // pass 2: (raw-unit threshold, raw-unit delta margin) per job
   uint32_t* counts;
   unsigned long long* job_kept;
-  uint2* slots;          // [n_items][4 warps][kSlots]: (job, u * nt + v) to re-score
-  uint8_t* slot_cnt;     // [n_items][4 warps]
+  uint2* slots;          // [n_items][epilogue warps][slots]: (job, u * nt + v) to re-score
+  uint8_t* slot_cnt;     // [n_items][epilogue warps]
   const float* qnorm;
   const float* kmax;  // per 128-token tile: max |k'_v|
   float kappa;
@@ -75,9 +79,22 @@ struct SParams {
 // Undecided pairs per (item, epilogue warp) kept for the exact re-score
 // without any global atomics; more than this (never seen in practice: the
 // mean is < 1 per warp) are decided in place.
-constexpr int kSlots = 8;
+#ifndef RP_SCORE_ABL
+#define RP_SCORE_ABL 0
+#endif
+constexpr int kSlotsPerItem = 32;
 
-constexpr int kThreads = 192;  // warps 0-3 epilogue (row = thread), 4 TMA, 5 MMA
+// Epilogue shape: 4 * CG warps, warp w reads TMEM lanes 32 (w % 4) .. (its
+// 32 rows) and column group w / 4 (128 / CG columns), so CG > 1 puts CG
+// warps on each sub-partition (latency hiding) and splits the per-row work.
+// Warp 4 CG issues TMA, warp 4 CG + 1 the MMAs.
+template <int CG>
+struct Epi {
+  static constexpr int kWarps = 4 * CG;
+  static constexpr int kThreads = 32 * (kWarps + 2);
+  static constexpr int kNW = 4 / CG;                    // 32-column words per warp
+  static constexpr int kSlots = kSlotsPerItem / kWarps;  // recheck slots per warp
+};
 constexpr int kChunkBytes = 128 * 128;
 
 template <int NC>
@@ -86,12 +103,13 @@ struct SLayout {
   static constexpr int kStages = 2;
   static constexpr int kSmemData = (1 + kStages) * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 6;
-  // bars | tmem slot (16 B) | (unused 512 B) | wcnt[4][128] | red[4][3] doubles
-  static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 4 * 128 * 4 + 4 * 3 * 8;
+  // bars | tmem slot (16 B) | (unused 512 B) | wcnt[4][128] | red[16][3] doubles
+  static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 4 * 128 * 4 + 16 * 3 * 8;
   static constexpr int kSmemBytes = kSmemData + kExtra + 1024;
 };
 
-RP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <int CG>
+RP_DEV void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * Epi<CG>::kWarps) : "memory"); }
 
 struct Welford {
   double n, mean, m2;
@@ -115,11 +133,41 @@ __device__ __noinline__ bool decide_exact(const SParams& p, const DJob& jb, int 
   return zscore(exact_score(p.feat, gr, kj + v), st) >= jb.param;
 }
 
-template <int NC, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+// Work order: units (one frame pair's items of one 128-token tile row, so
+// consecutive items share the Q' tile) are dealt round-robin to the CTAs.
+// The host sorts the units so that neighbouring units touch few frames:
+// all CTAs then work on a narrow window of Q / K frames at once and K
+// tiles come from L2 instead of HBM.
+struct UnitCursor {
+  const int2* units;
+  int n, u, it, hi;
+  RP_DEV explicit UnitCursor(const SParams& p)
+      : units(p.units), n(p.n_units), u(static_cast<int>(blockIdx.x)), it(0), hi(0) {
+    load();
+  }
+  RP_DEV void load() {
+    if (u < n) {
+      const int2 x = units[u];
+      it = x.x;
+      hi = x.y;
+    }
+  }
+  RP_DEV bool valid() const { return u < n; }
+  RP_DEV void next() {
+    if (++it >= hi) {
+      u += static_cast<int>(gridDim.x);
+      load();
+    }
+  }
+};
+
+template <int NC, int MODE, int CG>
+__global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
     score_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                  const SParams p) {
   using L = SLayout<NC>;
+  using E = Epi<CG>;
+  constexpr int kTma = E::kWarps, kMma = E::kWarps + 1, NW = E::kNW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -134,12 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_empty = q_full + 4;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
   uint32_t* wcnt = reinterpret_cast<uint32_t*>(tmem_slot + 4 + 128);  // [4][128]
-  double* red = reinterpret_cast<double*>(wcnt + 4 * 128);      // [4][3]
+  double* red = reinterpret_cast<double*>(wcnt + 4 * 128);      // [kWarps][3]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const long long per = (p.n_items + gridDim.x - 1) / gridDim.x;
-  const long long it0 = static_cast<long long>(blockIdx.x) * per;
-  const long long it1 = min(p.n_items, it0 + per);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < L::kStages; ++s) {
@@ -150,24 +195,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(q_empty, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 4);
+      mbar_init(&s_empty[b], E::kWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<256>(tmem_slot);
+  if (warp == kMma) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == kTma) {
     {
       // ------------------------------------------------------ TMA producer
       // (whole warp in uniform control flow, one elected lane issues)
       const uint64_t pol = policy_evict_normal();
       uint32_t kv_it = 0, qcnt = 0;
       int prev_tr = -1;
-      for (long long it = it0; it < it1; ++it) {
+      for (UnitCursor cur(p); cur.valid(); cur.next()) {
+        const long long it = cur.it;
         const int item_tr = shfl0(p.items[it].tr);
         const int item_tc = shfl0(p.items[it].tc);
         if (item_tr != prev_tr) {
@@ -190,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++kv_it;
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMma) {
     {
       // ------------------------------------------------------- MMA issuer
       // (whole warp: descriptors stay in uniform registers, see common.cuh)
@@ -198,7 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t qa = smem_u32(sq), kb0 = smem_u32(sk);
       uint32_t kv_it = 0, qcnt = 0, n = 0;
       int prev_tr = -1;
-      for (long long it = it0; it < it1; ++it, ++n) {
+      for (UnitCursor cur(p); cur.valid(); cur.next(), ++n) {
+        const long long it = cur.it;
         const int item_tr = shfl0(p.items[it].tr);
         const int item_tc = shfl0(p.items[it].tc);
         if (item_tr != prev_tr) {
@@ -214,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t kb = kb0 + st * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < NC * 4; ++kk) {
+        for (int kk = 0; kk < (RP_SCORE_ABL == 2 ? 1 : NC * 4); ++kk) {  // ABL 2: one MMA
           const uint32_t off = (kk / 4) * kChunkBytes + (kk % 4) * 32;
           umma_ss_w(tmem + buf * 128, smem_desc_sw128(qa + off, 0, 1024),
                   smem_desc_sw128(kb + off, 0, 1024), idesc, kk > 0);
@@ -231,21 +278,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // enough for the instruction cache (an earlier version that inlined the
     // exact re-score into every unrolled column ran at IPC 0.26, stalled on
     // instruction fetch).
-    const int r = warp * 32 + lane;  // row within the tile
-    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int rw = warp & 3, cg = warp >> 2;  // row group (TMEM lanes), column group
+    const int r = rw * 32 + lane;             // row within the tile
+    const int et = warp * 32 + lane;          // epilogue thread index
+    const uint32_t trow = tmem + (static_cast<uint32_t>(rw * 32) << 16) + cg * 32 * NW;
     uint32_t n = 0;
     // Item metadata is prefetched one item ahead (item -> job is a dependent
     // global load pair that would otherwise sit on every item's critical path).
     ScoreItem item_nx{};
     DJob jb_nx{};
-    if (it0 < it1) {
-      item_nx = p.items[it0];
+    UnitCursor nx(p);
+    if (nx.valid()) {
+      item_nx = p.items[nx.it];
       jb_nx = p.jobs[item_nx.job];
     }
-    for (long long it = it0; it < it1; ++it, ++n) {
+    for (UnitCursor cur(p); cur.valid(); cur.next(), ++n) {
+      const long long it = cur.it;
+      nx.next();
       const ScoreItem item = item_nx;
       const DJob jb = jb_nx;
-      if (it + 1 < it1) item_nx = p.items[it + 1];
+      if (nx.valid()) item_nx = p.items[nx.it];
       const long long gr = static_cast<long long>(item.tr) * 128 + r;
       float2 thr = make_float2(0.f, 0.f);
       float qk = 0.f;
@@ -255,15 +307,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint32_t buf = n & 1;
       mbar_wait(&s_full[buf], (n >> 1) & 1);
-      if (it + 1 < it1) jb_nx = p.jobs[item_nx.job];
+      if (nx.valid()) jb_nx = p.jobs[item_nx.job];
       tc_fence_after();
-      uint32_t sv[4][32];
+      uint32_t sv[NW][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(trow + buf * 128 + c * 32, sv[c]);
+      for (int c = 0; c < NW; ++c) tmem_ld32(trow + buf * 128 + c * 32, sv[c]);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[buf]);
+#if RP_SCORE_ABL == 1  // timing ablation only: no epilogue work
+      if (sv[0][0] == 0x7fffffffu && sv[NW - 1][31] == 0x7fffffffu) p.counts[0] = 1;
+      continue;
+#endif
       // valid columns of this row: contiguous [c_lo, c_hi] (band + frames)
       const long long qi = item.qi;
       const long long kj = item.kj;
@@ -275,19 +331,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         c_lo = static_cast<int>(max(kj + vlo - g0, 0ll));
         c_hi = static_cast<int>(min(kj + vhi - g0, 127ll));
       }
-      uint32_t inm[4];
+      uint32_t inm[NW];
+      int cnt = 0;
 #pragma unroll
-      for (int w4 = 0; w4 < 4; ++w4) {
-        const int lo = max(c_lo - 32 * w4, 0), hi = min(c_hi - 32 * w4, 31);
+      for (int w4 = 0; w4 < NW; ++w4) {
+        const int wb = 32 * (cg * NW + w4);
+        const int lo = max(c_lo - wb, 0), hi = min(c_hi - wb, 31);
         inm[w4] = lo > hi ? 0u : ((hi == 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+        cnt += __popc(inm[w4]);
       }
-      const int cnt = c_hi >= c_lo ? c_hi - c_lo + 1 : 0;
       if (MODE == 0) {
         // per-row sum and sum of squares of the valid scores (fp32, four
         // independent chains), then (n, sum, sumsq) reduced in fp64
         float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
+        for (int c = 0; c < 32 * NW; ++c) {
           const float x = (inm[c / 32] >> (c % 32)) & 1u
                               ? __uint_as_float(sv[c / 32][c % 32]) * p.score_scale : 0.f;
           a1[c & 3] += x;
@@ -307,10 +365,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           red[warp * 3 + 1] = t1;
           red[warp * 3 + 2] = t2;
         }
-        epi_bar();
-        if (r == 0) {
+        epi_bar<CG>();
+        if (et == 0) {
           double N = 0.0, S1 = 0.0, S2 = 0.0;
-          for (int x = 0; x < 4; ++x) {
+          for (int x = 0; x < E::kWarps; ++x) {
             N += red[3 * x];
             S1 += red[3 * x + 1];
             S2 += red[3 * x + 2];
@@ -320,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.item_stats[3 * it + 1] = mean;
           p.item_stats[3 * it + 2] = N > 0.0 ? fmax(S2 - S1 * mean, 0.0) : 0.0;
         }
-        epi_bar();
+        epi_bar<CG>();
       } else {
         // Decision thresholds of this row in raw accumulator units.  The
         // fast score differs from the reference's by at most
@@ -335,9 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float hi_raw = thr.x + m;
         const float lo_raw = thr.x - m;
         const double2 st = p.job_stats[item.job];  // for the rare exact decisions
-        uint32_t kb[4], ub[4];
+        uint32_t kb[NW], ub[NW];
 #pragma unroll
-        for (int w4 = 0; w4 < 4; ++w4) {
+        for (int w4 = 0; w4 < NW; ++w4) {
           uint32_t k1 = 0u, u1 = 0u;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -355,7 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // rare path: undecided pairs go to this (item, warp)'s slots for the
         // exact fp64 re-score (warp scan for the slot offsets, no atomics)
-        const int mine = __popc(ub[0]) + __popc(ub[1]) + __popc(ub[2]) + __popc(ub[3]);
+        int mine = 0;
+#pragma unroll
+        for (int w4 = 0; w4 < NW; ++w4) mine += __popc(ub[w4]);
         int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -363,18 +423,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane >= o) incl += y;
         }
         const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const long long sbase = (it * 4 + warp) * kSlots;
-        if (lane == 0) p.slot_cnt[it * 4 + warp] = static_cast<uint8_t>(min(total, kSlots));
+        const long long sbase = it * kSlotsPerItem + warp * E::kSlots;
+        if (lane == 0) p.slot_cnt[it * E::kWarps + warp] = static_cast<uint8_t>(min(total, E::kSlots));
         if (mine) {
           int at = incl - mine;
 #pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4) {
+          for (int w4 = 0; w4 < NW; ++w4) {
             uint32_t m = ub[w4];
             while (m) {
               const int i = __ffs(m) - 1;
               m &= m - 1;
-              const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 + 32 * w4 + i - kj);
-              if (at < kSlots)
+              const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 +
+                                             32 * (cg * NW + w4) + i - kj);
+              if (at < E::kSlots)
                 p.slots[sbase + at] = make_uint2(static_cast<uint32_t>(item.job),
                                                  static_cast<uint32_t>(u) * p.nt + v);
               else if (decide_exact(p, jb, v, gr, kj, st))
@@ -387,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (lane = row -> lane = column) and count
         unsigned long long kept_total = 0;
 #pragma unroll
-        for (int w4 = 0; w4 < 4; ++w4) {
+        for (int w4 = 0; w4 < NW; ++w4) {
           uint32_t x = kb[w4];
           kept_total += __popc(x);
 #pragma unroll
@@ -397,34 +458,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
             x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
           }
-          wcnt[warp * 128 + w4 * 32 + lane] = __popc(x);
+          wcnt[rw * 128 + (cg * NW + w4) * 32 + lane] = __popc(x);
         }
-        epi_bar();
-        // thread r owns column r: sum the warps of each block row
+        epi_bar<CG>();
+        // thread et < 128 owns column et: sum the row groups of each block row
         const int bs = p.bs;
         const int rows_per_blk = bs < 128 ? bs : 128;  // bs in {32, 64, 128}
-        const int wpb = rows_per_blk >> 5;             // warps per block row
-        const long long gc = static_cast<long long>(item.tc) * 128 + r;
-        for (int br = 0; br < 4 / wpb; ++br) {
-          uint32_t c2 = 0;
-          for (int x = 0; x < wpb; ++x) c2 += wcnt[(br * wpb + x) * 128 + r];
-          const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
-          const long long Cb = gc / bs;
-          const long long rr = R - jb.r0, cc = Cb - jb.c0;
-          if (rr >= 0 && rr < jb.tr && cc >= 0 && cc < jb.tc && c2)
-            p.counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs] = c2;
+        const int wpb = rows_per_blk >> 5;             // row groups per block row
+        if (et < 128) {
+          const long long gc = static_cast<long long>(item.tc) * 128 + et;
+          for (int br = 0; br < 4 / wpb; ++br) {
+            uint32_t c2 = 0;
+            for (int x = 0; x < wpb; ++x) c2 += wcnt[(br * wpb + x) * 128 + et];
+            const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
+            const long long Cb = gc / bs;
+            const long long rr = R - jb.r0, cc = Cb - jb.c0;
+            if (rr >= 0 && rr < jb.tr && cc >= 0 && cc < jb.tc && c2)
+              p.counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs] = c2;
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) kept_total += __shfl_xor_sync(0xFFFFFFFFu, kept_total, o);
         if (lane == 0 && kept_total) atomicAdd(&p.job_kept[item.job], kept_total);
-        epi_bar();  // wcnt reuse
+        epi_bar<CG>();  // wcnt reuse
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMma) {
     tc_fence_after();
     tmem_dealloc<256>(tmem);
   }
@@ -489,14 +552,14 @@ __global__ void recheck_kernel(const DJob* __restrict__ jobs, const uint2* __res
                                const uint8_t* __restrict__ slot_cnt, long long groups, Feat f,
                                const double2* __restrict__ job_stats, uint32_t* counts,
                                unsigned long long* job_kept, unsigned long long* rechecked,
-                               int nt, int bs) {
+                               int nt, int bs, int slots_per_group) {
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < groups;
        x += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int n = slot_cnt[x];
     if (!n) continue;
     atomicAdd(rechecked, static_cast<unsigned long long>(n));
     for (int e = 0; e < n; ++e) {
-      const uint2 sl = slots[x * kSlots + e];
+      const uint2 sl = slots[x * slots_per_group + e];
       const DJob& jb = jobs[sl.x];
       const int64_t u = sl.y / nt, v = sl.y % nt;
       const float s = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
@@ -590,11 +653,13 @@ class FastEngine {
   int cmin = 0, amin = 0, heads = 0, dim = 0, nc = 0;
   std::vector<DJob> jobs;        // score jobs only (cnt_off set)
   std::vector<ScoreItem> items;
+  std::vector<int2> units;       // item ranges of one (job, tile row), locality order
   std::vector<long long> job_item_off;
   std::vector<Item> tiles;       // block tiles of every score job (apply)
   int64_t ncounts = 0;
   DJob* d_jobs = nullptr;
   ScoreItem* d_items = nullptr;
+  int2* d_units = nullptr;
   long long* d_job_item_off = nullptr;
   Item* d_tiles = nullptr;
   uint32_t* d_counts = nullptr;
@@ -611,6 +676,7 @@ class FastEngine {
   ~FastEngine() {
     for (void* p : {static_cast<void*>(d_jobs), static_cast<void*>(d_items),
                     static_cast<void*>(d_job_item_off), static_cast<void*>(d_tiles),
+                    static_cast<void*>(d_units),
                     static_cast<void*>(d_counts), static_cast<void*>(d_item_stats),
                     static_cast<void*>(d_job_stats), static_cast<void*>(d_kept),
                     static_cast<void*>(d_job_thr),
@@ -678,9 +744,35 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
   }
   e->job_item_off.push_back(static_cast<long long>(e->items.size()));
   e->ncounts = off;
+  // units: runs of items with the same (job, tile row)
+  for (size_t a = 0; a < e->items.size();) {
+    size_t b = a + 1;
+    while (b < e->items.size() && e->items[b].job == e->items[a].job &&
+           e->items[b].tr == e->items[a].tr)
+      ++b;
+    e->units.push_back(make_int2(static_cast<int>(a), static_cast<int>(b)));
+    a = b;
+  }
+  // Locality order: frame pairs in F x F blocks of (key frame, query frame),
+  // F chosen so the block's Q' and K' frames (2 F frames of heads * d bf16
+  // per token) stay well inside L2; concurrent CTAs then share K tiles.
+  {
+    const double frame_bytes = static_cast<double>(nt) * heads * head_dim * 2.0;
+    const int F = std::max(1, static_cast<int>((32.0 * (1 << 20)) / (2.0 * frame_bytes)));
+    auto key = [&](const int2& u) {
+      const ScoreItem& it = e->items[u.x];
+      const DJob& d = e->jobs[it.job];
+      return std::make_tuple(d.j / F, d.i / F, d.j, d.i, it.tr);
+    };
+    const char* order = std::getenv("DYNRAD_SCORE_ORDER");  // "plain": item order (A/B)
+    if (!(order && std::strcmp(order, "plain") == 0))
+      std::stable_sort(e->units.begin(), e->units.end(),
+                       [&](const int2& a, const int2& b) { return key(a) < key(b); });
+  }
   const size_t nj = e->jobs.size();
   dalloc(&e->d_jobs, nj);
   dalloc(&e->d_items, e->items.size());
+  dalloc(&e->d_units, e->units.size());
   dalloc(&e->d_job_item_off, nj + 1);
   dalloc(&e->d_tiles, e->tiles.size());
   dalloc(&e->d_counts, static_cast<size_t>(off));
@@ -688,13 +780,15 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
   dalloc(&e->d_job_stats, nj);
   dalloc(&e->d_job_thr, nj);
   dalloc(&e->d_kept, nj + 1);
-  dalloc(&e->d_slots, e->items.size() * 4 * kSlots);
-  dalloc(&e->d_slot_cnt, e->items.size() * 4);
+  dalloc(&e->d_slots, e->items.size() * kSlotsPerItem);
+  dalloc(&e->d_slot_cnt, e->items.size() * 16);  // up to 16 epilogue warps
   dalloc(&e->d_qn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kmax, static_cast<size_t>((g.padded_tokens + 127) / 128));
   RP_CUDA(cudaMemcpy(e->d_jobs, e->jobs.data(), sizeof(DJob) * nj, cudaMemcpyHostToDevice));
   RP_CUDA(cudaMemcpy(e->d_items, e->items.data(), sizeof(ScoreItem) * e->items.size(),
+                     cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(e->d_units, e->units.data(), sizeof(int2) * e->units.size(),
                      cudaMemcpyHostToDevice));
   RP_CUDA(cudaMemcpy(e->d_job_item_off, e->job_item_off.data(), sizeof(long long) * (nj + 1),
                      cudaMemcpyHostToDevice));
@@ -705,28 +799,53 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
 
 void fast_engine_destroy(FastEngine* e) { delete e; }
 
-template <int NC>
-static void launch_pass(const CUtensorMap& mq, const CUtensorMap& mk, const SParams& p, int mode,
-                        int grid, cudaStream_t s) {
+template <int NC, int CG>
+static void launch_pass_cg(const CUtensorMap& mq, const CUtensorMap& mk, const SParams& p,
+                           int mode, int grid, cudaStream_t s) {
   const int smem = SLayout<NC>::kSmemBytes;
+  const int threads = Epi<CG>::kThreads;
   if (mode == 0) {
     static bool attr = false;
     if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 0>,
+      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 0, CG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
-    score_kernel<NC, 0><<<grid, kThreads, smem, s>>>(mq, mk, p);
+    score_kernel<NC, 0, CG><<<grid, threads, smem, s>>>(mq, mk, p);
   } else {
     static bool attr = false;
     if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 1>,
+      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 1, CG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
-    score_kernel<NC, 1><<<grid, kThreads, smem, s>>>(mq, mk, p);
+    score_kernel<NC, 1, CG><<<grid, threads, smem, s>>>(mq, mk, p);
   }
   RP_LAUNCHED();
+}
+
+// Epilogue column groups (warps per sub-partition, see Epi) per pass.
+// Measured at the Hunyuan shape (profiles/r1_score_ablation.md): the stats
+// pass is feed-bound and runs best with CG = 1; the select pass's longer
+// epilogue gains ~9 % from two warps per sub-partition.  DYNRAD_SCORE_CG in
+// {1, 2, 4} forces both.
+static int score_cg(int mode) {
+  static const int forced = [] {
+    const char* e = std::getenv("DYNRAD_SCORE_CG");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 1 || v == 2 || v == 4) ? v : 0;
+  }();
+  return forced ? forced : (mode == 0 ? 1 : 2);
+}
+
+template <int NC>
+static void launch_pass(const CUtensorMap& mq, const CUtensorMap& mk, const SParams& p, int mode,
+                        int grid, cudaStream_t s) {
+  switch (score_cg(mode)) {
+    case 1: launch_pass_cg<NC, 1>(mq, mk, p, mode, grid, s); break;
+    case 4: launch_pass_cg<NC, 4>(mq, mk, p, mode, grid, s); break;
+    default: launch_pass_cg<NC, 2>(mq, mk, p, mode, grid, s); break;
+  }
 }
 
 void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, const Feat& f,
@@ -760,6 +879,8 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.jobs = e->d_jobs;
   p.items = e->d_items;
   p.n_items = static_cast<long long>(e->items.size());
+  p.units = e->d_units;
+  p.n_units = static_cast<int>(e->units.size());
   p.nt = g.tokens_per_frame;
   p.bs = g.block_size;
   p.cph = e->dim / 64;
@@ -782,7 +903,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   int dev = 0, sms = 0;
   RP_CUDA(cudaGetDevice(&dev));
   RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = static_cast<int>(std::min<long long>(p.n_items, sms));
+  const int grid = std::min(p.n_units, sms);
   for (int mode = 0; mode < 2; ++mode) {
     switch (e->nc) {
       case 1: launch_pass<1>(mq, mk, p, mode, grid, s); break;
@@ -799,11 +920,12 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   }
   // exact re-score of the pairs within their error bound of tau
   {
-    const long long groups = static_cast<long long>(e->items.size()) * 4;
+    const int ew = 4 * score_cg(1);  // slots are written by the select pass
+    const long long groups = static_cast<long long>(e->items.size()) * ew;
     recheck_kernel<<<static_cast<unsigned>(std::min<long long>((groups + 255) / 256, sms * 16)),
                      256, 0, s>>>(e->d_jobs, e->d_slots, e->d_slot_cnt, groups, f,
                                   e->d_job_stats, e->d_counts, e->d_kept, e->d_kept + nj,
-                                  g.tokens_per_frame, g.block_size);
+                                  g.tokens_per_frame, g.block_size, kSlotsPerItem / ew);
     RP_LAUNCHED();
   }
   // fallback_k: only when it can activate a column (fallback_k >= cmin)
