@@ -202,3 +202,35 @@ def test_hunyuan_dynamic_fast_engine_equals_exact_engine(cuda):
     exact = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=2)).build_mask_device(q, k, 2)
     assert st["scored_pairs"] == 7864099452
     assert torch.equal(fast, exact)
+
+
+_SCHEDULE_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2604_20470_b200 import radialplan as rp
+g = rp.make_grid(8, 512, 64)
+cfg = rp.SparsityConfig(rp.Mode.DynamicThreshold, rp.RadialParams(1.4, 0.7), 0.7, 0.45, -1.5, 2.0)
+gen = torch.Generator(device="cuda").manual_seed(5)
+q = torch.randn((g.total_tokens, 4, 128), device="cuda", generator=gen).to(torch.bfloat16)
+k = torch.randn((g.total_tokens, 4, 128), device="cuda", generator=gen).to(torch.bfloat16)
+fast = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=1)).build_mask_device(q, k, 2)
+exact = rp.Plan(g, cfg, 7, rp.BuildOptions(score_engine=2)).build_mask_device(q, k, 2)
+assert torch.equal(fast, exact)
+print("OK", int(fast.sum()))
+"""
+
+
+@pytest.mark.parametrize("env", [{"DYNRAD_SCORE_CG": "1"}, {"DYNRAD_SCORE_CG": "2"},
+                                 {"DYNRAD_SCORE_CG": "4"}, {"DYNRAD_SCORE_ORDER": "plain"}],
+                         ids=lambda e: "-".join(f"{k}={v}" for k, v in e.items()))
+def test_fast_engine_schedules_are_exact(cuda, env):
+    """Every epilogue width (warps per sub-partition) and work order of the
+    tensor-core scorer gives the exact engine's mask (read once per process,
+    so each runs in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _SCHEDULE_SCRIPT, root], capture_output=True,
+                       text=True, timeout=300, env={**os.environ, **env})
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
