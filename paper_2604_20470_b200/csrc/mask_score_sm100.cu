@@ -283,31 +283,49 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
     const int et = warp * 32 + lane;          // epilogue thread index
     const uint32_t trow = tmem + (static_cast<uint32_t>(rw * 32) << 16) + cg * 32 * NW;
     uint32_t n = 0;
-    // Item metadata is prefetched one item ahead (item -> job is a dependent
-    // global load pair that would otherwise sit on every item's critical path).
-    ScoreItem item_nx{};
-    DJob jb_nx{};
-    UnitCursor nx(p);
-    if (nx.valid()) {
-      item_nx = p.items[nx.it];
-      jb_nx = p.jobs[item_nx.job];
+    // Item metadata is software-pipelined: item n + 2 is loaded while item n
+    // is processed, and the loads that depend on it (its frame pair, the
+    // pass-2 threshold, |q'| of the row, max |k'| of the tile) one item
+    // later, so no global-load latency sits on an item's critical path.
+    ScoreItem itm0{}, itm1{};
+    DJob jb0{};
+    float2 thr0 = make_float2(0.f, 0.f);
+    float qn0 = 0.f, km0 = 0.f;
+    auto job_loads = [&](const ScoreItem& x) {
+      jb0 = p.jobs[x.job];
+      if (MODE == 1) {
+        thr0 = p.job_thr[x.job];
+        qn0 = __ldg(p.qnorm + static_cast<long long>(x.tr) * 128 + r);
+        km0 = __ldg(p.kmax + x.tc);
+      }
+    };
+    UnitCursor ahead(p);
+    if (ahead.valid()) {
+      itm0 = p.items[ahead.it];
+      job_loads(itm0);
+      ahead.next();
+    }
+    bool has1 = ahead.valid();
+    if (has1) {
+      itm1 = p.items[ahead.it];
+      ahead.next();
     }
     for (UnitCursor cur(p); cur.valid(); cur.next(), ++n) {
       const long long it = cur.it;
-      nx.next();
-      const ScoreItem item = item_nx;
-      const DJob jb = jb_nx;
-      if (nx.valid()) item_nx = p.items[nx.it];
-      const long long gr = static_cast<long long>(item.tr) * 128 + r;
-      float2 thr = make_float2(0.f, 0.f);
-      float qk = 0.f;
-      if (MODE == 1) {
-        thr = p.job_thr[item.job];
-        qk = __ldg(p.qnorm + gr) * p.kappa * __ldg(p.kmax + item.tc);
+      const ScoreItem item = itm0;
+      const DJob jb = jb0;
+      const float2 thr = thr0;
+      const float qk = qn0 * p.kappa * km0;
+      if (has1) job_loads(itm1);
+      itm0 = itm1;
+      has1 = ahead.valid();
+      if (has1) {
+        itm1 = p.items[ahead.it];
+        ahead.next();
       }
+      const long long gr = static_cast<long long>(item.tr) * 128 + r;
       const uint32_t buf = n & 1;
       mbar_wait(&s_full[buf], (n >> 1) & 1);
-      if (nx.valid()) jb_nx = p.jobs[item_nx.job];
       tc_fence_after();
       uint32_t sv[NW][32];
 #pragma unroll
@@ -344,12 +362,17 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
         // per-row sum and sum of squares of the valid scores (fp32, four
         // independent chains), then (n, sum, sumsq) reduced in fp64
         float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+        // 32-column words outside the band / frame for the whole warp are
+        // skipped (they would add zeros: same sums bit for bit)
 #pragma unroll
-        for (int c = 0; c < 32 * NW; ++c) {
-          const float x = (inm[c / 32] >> (c % 32)) & 1u
-                              ? __uint_as_float(sv[c / 32][c % 32]) * p.score_scale : 0.f;
-          a1[c & 3] += x;
-          a2[c & 3] = fmaf(x, x, a2[c & 3]);
+        for (int w4 = 0; w4 < NW; ++w4) {
+          if (!__any_sync(0xFFFFFFFFu, inm[w4] != 0u)) continue;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = (inm[w4] >> i) & 1u ? __uint_as_float(sv[w4][i]) * p.score_scale : 0.f;
+            a1[i & 3] += x;
+            a2[i & 3] = fmaf(x, x, a2[i & 3]);
+          }
         }
         double t1 = static_cast<double>((a1[0] + a1[1]) + (a1[2] + a1[3]));
         double t2 = static_cast<double>((a2[0] + a2[1]) + (a2[2] + a2[3]));
@@ -392,13 +415,15 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
         const float m = fmaf(qk, 1.f + 0x1p-20f, thr.y) + 0x1p-20f * fabsf(thr.x);
         const float hi_raw = thr.x + m;
         const float lo_raw = thr.x - m;
-        const double2 st = p.job_stats[item.job];  // for the rare exact decisions
         uint32_t kb[NW], ub[NW];
 #pragma unroll
         for (int w4 = 0; w4 < NW; ++w4) {
           uint32_t k1 = 0u, u1 = 0u;
+          // words empty for the whole warp (band edge, frame boundary) skip
+          // the compares
+          const bool any = __any_sync(0xFFFFFFFFu, inm[w4] != 0u);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < 32 && any; ++i) {
             // compare + predicated OR per mask (2 instructions per bit)
             asm("{\n\t.reg .pred pk, pu;\n\t"
                 "setp.ge.f32 pk, %2, %3;\n\t"
@@ -438,7 +463,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
               if (at < E::kSlots)
                 p.slots[sbase + at] = make_uint2(static_cast<uint32_t>(item.job),
                                                  static_cast<uint32_t>(u) * p.nt + v);
-              else if (decide_exact(p, jb, v, gr, kj, st))
+              else if (decide_exact(p, jb, v, gr, kj, p.job_stats[item.job]))
                 kb[w4] |= 1u << i;
               ++at;
             }
