@@ -103,8 +103,9 @@ struct SLayout {
   static constexpr int kStages = 2;
   static constexpr int kSmemData = (1 + kStages) * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 6;
-  // bars | tmem slot (16 B) | (unused 512 B) | wcnt[4][128] | red[16][3] doubles
-  static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 4 * 128 * 4 + 16 * 3 * 8;
+  // bars | tmem slot (16 B) | (unused 512 B) | wcnt[2][4][128] | red[2][16][3] doubles
+  // (wcnt / red double-buffered by item parity: one epilogue barrier per item)
+  static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 2 * 4 * 128 * 4 + 2 * 16 * 3 * 8;
   static constexpr int kSmemBytes = kSmemData + kExtra + 1024;
 };
 
@@ -181,8 +182,8 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
   uint64_t* s_full = q_full + 2;   // [2]
   uint64_t* s_empty = q_full + 4;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(tmem_slot + 4 + 128);  // [4][128]
-  double* red = reinterpret_cast<double*>(wcnt + 4 * 128);      // [kWarps][3]
+  uint32_t* wcnt_base = reinterpret_cast<uint32_t*>(tmem_slot + 4 + 128);  // [2][4][128]
+  double* red_base = reinterpret_cast<double*>(wcnt_base + 2 * 4 * 128);  // [2][16][3]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
           t2 += __shfl_xor_sync(0xFFFFFFFFu, t2, o);
           tn += __shfl_xor_sync(0xFFFFFFFFu, tn, o);
         }
+        double* red = red_base + (n & 1) * 16 * 3;
         if (lane == 0) {
           red[warp * 3 + 0] = tn;
           red[warp * 3 + 1] = t1;
@@ -401,7 +403,8 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
           p.item_stats[3 * it + 1] = mean;
           p.item_stats[3 * it + 2] = N > 0.0 ? fmax(S2 - S1 * mean, 0.0) : 0.0;
         }
-        epi_bar<CG>();
+        // no trailing barrier: the next item writes the other red buffer, and
+        // this one is rewritten only after the next item's barrier
       } else {
         // Decision thresholds of this row in raw accumulator units.  The
         // fast score differs from the reference's by at most
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
             const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
             x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
           }
-          wcnt[rw * 128 + (cg * NW + w4) * 32 + lane] = __popc(x);
+          wcnt_base[(n & 1) * 512 + rw * 128 + (cg * NW + w4) * 32 + lane] = __popc(x);
         }
         epi_bar<CG>();
         // thread et < 128 owns column et: sum the row groups of each block row
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
           const long long gc = static_cast<long long>(item.tc) * 128 + et;
           for (int br = 0; br < 4 / wpb; ++br) {
             uint32_t c2 = 0;
-            for (int x = 0; x < wpb; ++x) c2 += wcnt[(br * wpb + x) * 128 + et];
+            for (int x = 0; x < wpb; ++x) c2 += wcnt_base[(n & 1) * 512 + (br * wpb + x) * 128 + et];
             const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
             const long long Cb = gc / bs;
             const long long rr = R - jb.r0, cc = Cb - jb.c0;
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) kept_total += __shfl_xor_sync(0xFFFFFFFFu, kept_total, o);
         if (lane == 0 && kept_total) atomicAdd(&p.job_kept[item.job], kept_total);
-        epi_bar<CG>();  // wcnt reuse
+        // no trailing barrier (wcnt is double-buffered, see red above)
       }
     }
   }
