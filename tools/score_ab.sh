@@ -3,11 +3,11 @@
 # in-tree libdynrad.so and variants/$1.so, plus one ncu launch list each.
 mkdir -p gpurun_out
 for r in 1 2 3; do
-  echo "== new";  timeout 200 python tools/dyn_stats.py | grep hunyuan | grep -o "build ms.*"
-  echo "== $1"; DYNRAD_LIB=$PWD/variants/$1.so timeout 200 python tools/dyn_stats.py | grep hunyuan | grep -o "build ms.*"
+  echo "== new";  timeout 200 python tools/dyn_stats.py | grep hunyuan | grep -o "rechecked_pairs[^,]*\|build ms.*"
+  echo "== $1"; DYNRAD_LIB=$PWD/variants/$1.so timeout 200 python tools/dyn_stats.py | grep hunyuan | grep -o "rechecked_pairs[^,]*\|build ms.*"
 done
 for v in new $1; do
   echo "== ncu $v"
   if [ $v = new ]; then L=; else L=DYNRAD_LIB=$PWD/variants/$v.so; fi
-  env $L timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:score_kernel -c 2 --csv python tools/dyn_stats.py 2>/dev/null | grep score_kernel | awk -F'","' '{print $5, $NF}' | cut -c1-120
+  env $L timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"score_kernel|recheck_kernel" -c 3 --csv python tools/dyn_stats.py 2>/dev/null | grep -E "score_kernel|recheck_kernel" | awk -F'","' '{print substr($5,1,40), $NF}'
 done
