@@ -555,11 +555,17 @@ def main():
                "sample": desc, "sample_wall_s": dt}
 
     traffic = None
-    rpk = os.environ.get("DYNRAD_K6") == "rp"
+    # stage-(d) kernel: DYNRAD_K6 if set, else the library's auto rule (rp once
+    # one head's K + V exceed 64 MiB, see capi.cu launch_attention)
+    forced = os.environ.get("DYNRAD_K6")
+    rpk = forced == "rp" or (forced is None and 4 * g.padded_tokens * 128 > 64 * 2**20)
     kname = "bsfa_fwd_rp_kernel<128> (row pairs)" if rpk else "bsfa_fwd_db_kernel<128>"
-    prof = os.path.join(ROOT, "profiles", "k6db_ncu_summary.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
+    # DRAM traffic per launch from the one ncu --set full capture of this
+    # kernel at this config (null when none was taken)
+    prof = {("wan_static", False): "k6db_ncu_summary.json",
+            ("hunyuan_dynamic", True): "k6rp_hunyuan_ncu_summary.json"}.get((args.config, rpk))
+    if prof and os.path.exists(os.path.join(ROOT, "profiles", prof)):
+        with open(os.path.join(ROOT, "profiles", prof)) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
 
     peak = peaks["bf16_tflops"]

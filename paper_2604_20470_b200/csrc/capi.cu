@@ -90,22 +90,31 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (t->token_stride % 8 || t->head_stride % 8)
         throw std::invalid_argument("sparse attention (bf16): strides must be multiples of 8");
     const CUtensorMap mq = make_map_bf16(q), mk = make_map_bf16(k), mv = make_map_bf16(v);
-    // K6 variant (DYNRAD_K6): "db" (default) = one query tile per CTA,
+    // K6 variant (DYNRAD_K6, default auto: see below): "db" = one query tile per CTA,
     // score tile double-buffered in TMEM, Q in TMEM (attn_sm100_db.cu);
     // "rp" = block-row pairs of one head sharing every K/V tile
     // (attn_sm100_rp.cu: fastest on dense / long shared lists).  Measured side
     // by side in DESIGN.md section 8.
     // "rp2" = row pairs sharing K/V with a double-buffered score tile per
     // query tile at half-block granularity (attn_sm100_rp2.cu).
-    static const int variant = [] {
+    static const int forced = [] {
       const char* e = std::getenv("DYNRAD_K6");
       if (e && std::strcmp(e, "rp") == 0) return 0;
+      if (e && std::strcmp(e, "db") == 0) return 1;
       if (e && std::strcmp(e, "rp2") == 0) return 2;
       if (e && std::strcmp(e, "alt") == 0) return 3;
       if (e && std::strcmp(e, "cta2") == 0) return 5;
       if (e && std::strcmp(e, "mc") == 0) return 6;
-      return 1;
+      return -1;  // auto
     }();
+    // auto: db while one head's K and V fit comfortably in L2 (the natural
+    // row order then shares K/V tiles between concurrent CTAs through L2);
+    // rp once they do not (it reuses every K/V tile for two block rows in
+    // the CTA).  Measured: Wan 75.8 k tokens (38.8 MB K+V per head) db
+    // 22.4 ms vs rp 24.2 ms; Hunyuan 219.6 k tokens (112 MB) db 109.2 ms vs
+    // rp 105.1 ms.
+    const double kv_head_bytes = 4.0 * static_cast<double>(g.padded_tokens) * d;
+    const int variant = forced >= 0 ? forced : (kv_head_bytes > 64.0 * (1 << 20) ? 0 : 1);
     // The kernels re-balance registers between warpgroups with setmaxnreg;
     // that only works if the launch allocates the full 168 x 384 pool.
     auto check_regs = [](const void* fn) {

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("variant", ["rp", "rp2", "alt", "cta2", "mc"])
+@pytest.mark.parametrize("variant", ["db", "rp", "rp2", "alt", "cta2", "mc"])
 def test_variant_passes_attention_parity(cuda, variant):
     env = dict(os.environ, DYNRAD_K6=variant)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
