@@ -108,6 +108,15 @@ typedef struct {
   int64_t head_stride;  /* elements between consecutive heads */
 } rp_tensor;
 
+/* random_batch (attention.hpp:62-63, attention.cpp:182-204) on the device:
+ * the reference's counter-based synthetic features.  Writes heads
+ * [first_head, first_head + heads) of the reference's batch into q / k / v
+ * (each may be NULL; [tokens, heads, head_dim] f32 or bf16 -- bf16 is the
+ * round-to-nearest-even of the reference's float).  head_dim % 8 == 0. */
+rp_status rp_random_batch(int64_t tokens, int heads, int head_dim, uint64_t seed,
+                          int first_head, rp_tensor* q, rp_tensor* k, rp_tensor* v,
+                          rp_stream stream);
+
 /* ------------------------------------------------------------ mask build --
  * radialplan::build_mask (mask.hpp:88-89, mask.cpp:162-289): stages (a)
  * candidates, (b) proxy scoring, (c) selection + theta_c/theta_m block
@@ -274,6 +283,24 @@ rp_status rp_sparse_attention_fwd(const rp_grid* g, const rp_tensor* q,
                                   const int32_t* col_idx_dev,
                                   const int32_t* row_order_dev,
                                   float softmax_scale, rp_stream stream);
+
+/* Same, plus the reference's empty-row check (attention.cpp:85-86 throws
+ * std::domain_error when a row has no active key): rows without an active
+ * block are zero-filled and *err_flag_dev (device int, caller-zeroed; may be
+ * NULL) is set to 1.  Stream-ordered: the caller reads the flag after the
+ * stream and raises RP_DOMAIN_ERROR / domain_error itself. */
+rp_status rp_sparse_attention_fwd_checked(const rp_grid* g, const rp_tensor* q,
+                                          const rp_tensor* k, const rp_tensor* v,
+                                          rp_tensor* o, const int32_t* row_ptr_dev,
+                                          const int32_t* col_idx_dev,
+                                          const int32_t* row_order_dev,
+                                          float softmax_scale, int* err_flag_dev,
+                                          rp_stream stream);
+
+/* Name of the stage-(d) kernel rp_sparse_attention_fwd launches for this
+ * grid, dtype (rp_dtype) and head_dim.  bf16: "db" while one head's K + V
+ * fit in 64 MiB, "rp" above (DYNRAD_K6 = db | rp forces one per process). */
+const char* rp_attention_kernel(const rp_grid* g, int dtype, int head_dim);
 
 /* Host-buffer convenience with the reference's calling convention: host
  * Q/K/V [tokens, heads, d] (pinned or pageable; dtype f32 or bf16), host

@@ -153,6 +153,11 @@ _SIGS = {
     "rp_mask_sparsity": ([_P(Grid), _v, _P(C.c_int64), _P(C.c_double), _v], C.c_int),
     "rp_sparse_attention_fwd": ([_P(Grid), _P(Tensor), _P(Tensor), _P(Tensor), _P(Tensor), _v,
                                  _v, _v, C.c_float, _v], C.c_int),
+    "rp_sparse_attention_fwd_checked": ([_P(Grid), _P(Tensor), _P(Tensor), _P(Tensor),
+                                         _P(Tensor), _v, _v, _v, C.c_float, _v, _v], C.c_int),
+    "rp_attention_kernel": ([_P(Grid), C.c_int, C.c_int], C.c_char_p),
+    "rp_random_batch": ([C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, _P(Tensor),
+                         _P(Tensor), _P(Tensor), _v], C.c_int),
     "rp_masked_attention_exact_host": ([_P(Grid), _v, _v, _v, _v, C.c_int, C.c_int64, C.c_int,
                                         C.c_int, _v, _v], C.c_int),
     "rp_soft_attention_fwd": ([_P(Grid), _P(Tensor), _P(Tensor), _P(Tensor), _P(Tensor), _v,
@@ -176,7 +181,6 @@ _SIGS = {
     "rp_pooled_select": ([_P(Grid), _P(Config), _P(Tensor), _P(Tensor), C.c_int, C.c_int,
                           C.c_double, _v, _v], C.c_int),
     "rp_block_mean_pool": ([_P(Grid), _P(Tensor), C.c_int, _v, _v], C.c_int),
-    "rp_debug_umma_probe": ([_v, _v, _v, _v, _v, _v, _v], C.c_int),
 }
 
 # Every symbol include/dynrad.h declares (the CPU tests check the exports).

@@ -18,14 +18,10 @@
 // Pull in the kernel definitions (single translation unit keeps template
 // instantiation and the launch sites together).
 #include "attn_f32.cu"
-#include "umma_probe.cu"
 #include "attn_sm100_db.cu"
 #include "attn_sm100_rp.cu"
-#include "attn_sm100_rp2.cu"
-#include "attn_sm100_alt.cu"
-#include "attn_sm100_2cta.cu"
-#include "attn_sm100_mc.cu"
 #include "csr.cu"
+#include "random_batch.cu"
 
 namespace rp {
 
@@ -70,6 +66,59 @@ static bool use_lpt_order() {
   return lpt;
 }
 
+// Stage-(d) kernel.  "db" (attn_sm100_db.cu): one query tile per CTA, score
+// tile double-buffered in TMEM, Q in TMEM, two softmax warps per row.  "rp"
+// (attn_sm100_rp.cu): block-row pairs of one head sharing every K/V tile
+// over their union list.  DYNRAD_K6=db|rp forces one; the default (auto) is
+// db while one head's K + V fit in half of L2 and rp above that (measured:
+// Wan 75.8 k tokens, 38.8 MB per head: db 22.4 ms vs rp 24.2 ms; Hunyuan
+// 219.6 k tokens, 112 MB: db 109.2 ms vs rp 105.1 ms).
+// Measured alternatives (incl. round 2's two-tile ping-pong "pp") live in
+// tools/experiments/k6_variants/.
+enum class K6Variant { kAuto, kDB, kRP };
+static K6Variant k6_forced() {
+  static const K6Variant v = [] {
+    const char* e = std::getenv("DYNRAD_K6");
+    if (e && std::strcmp(e, "db") == 0) return K6Variant::kDB;
+    if (e && std::strcmp(e, "rp") == 0) return K6Variant::kRP;
+    return K6Variant::kAuto;
+  }();
+  return v;
+}
+static K6Variant k6_variant(int64_t padded_tokens, int head_dim) {
+  const K6Variant f = k6_forced();
+  if (f != K6Variant::kAuto) return f;
+  const double kv_head_bytes = 4.0 * static_cast<double>(padded_tokens) * head_dim;
+  return kv_head_bytes > 64.0 * (1 << 20) ? K6Variant::kRP : K6Variant::kDB;
+}
+static const char* k6_kernel_name(int64_t padded_tokens, int head_dim) {
+  if (k6_variant(padded_tokens, head_dim) == K6Variant::kRP)
+    return head_dim == 64 ? "bsfa_fwd_rp_kernel<64>" : "bsfa_fwd_rp_kernel<128>";
+  return head_dim == 64 ? "bsfa_fwd_db_kernel<64>" : "bsfa_fwd_db_kernel<128>";
+}
+
+// Large-shared-memory opt-in is a per-(kernel, device) attribute: remember
+// which devices each kernel was prepared on (bit = device ordinal).
+void prepare_kernel(const void* fn, int smem, void (*check)(const void*)) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, uint64_t>> done;
+  int dev = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t{1} << (dev & 63);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : done)
+    if (e.first == fn) {
+      if (e.second & bit) return;
+      if (check) check(fn);
+      RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      e.second |= bit;
+      return;
+    }
+  if (check) check(fn);
+  RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  done.emplace_back(fn, bit);
+}
+
 static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tensor& k,
                              const rp_tensor& v, rp_tensor& o, const int32_t* row_ptr,
                              const int32_t* col_idx, const int32_t* row_order, float scale,
@@ -90,31 +139,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (t->token_stride % 8 || t->head_stride % 8)
         throw std::invalid_argument("sparse attention (bf16): strides must be multiples of 8");
     const CUtensorMap mq = make_map_bf16(q), mk = make_map_bf16(k), mv = make_map_bf16(v);
-    // K6 variant (DYNRAD_K6, default auto: see below): "db" = one query tile per CTA,
-    // score tile double-buffered in TMEM, Q in TMEM (attn_sm100_db.cu);
-    // "rp" = block-row pairs of one head sharing every K/V tile
-    // (attn_sm100_rp.cu: fastest on dense / long shared lists).  Measured side
-    // by side in DESIGN.md section 8.
-    // "rp2" = row pairs sharing K/V with a double-buffered score tile per
-    // query tile at half-block granularity (attn_sm100_rp2.cu).
-    static const int forced = [] {
-      const char* e = std::getenv("DYNRAD_K6");
-      if (e && std::strcmp(e, "rp") == 0) return 0;
-      if (e && std::strcmp(e, "db") == 0) return 1;
-      if (e && std::strcmp(e, "rp2") == 0) return 2;
-      if (e && std::strcmp(e, "alt") == 0) return 3;
-      if (e && std::strcmp(e, "cta2") == 0) return 5;
-      if (e && std::strcmp(e, "mc") == 0) return 6;
-      return -1;  // auto
-    }();
-    // auto: db while one head's K and V fit comfortably in L2 (the natural
-    // row order then shares K/V tiles between concurrent CTAs through L2);
-    // rp once they do not (it reuses every K/V tile for two block rows in
-    // the CTA).  Measured: Wan 75.8 k tokens (38.8 MB K+V per head) db
-    // 22.4 ms vs rp 24.2 ms; Hunyuan 219.6 k tokens (112 MB) db 109.2 ms vs
-    // rp 105.1 ms.
-    const double kv_head_bytes = 4.0 * static_cast<double>(g.padded_tokens) * d;
-    const int variant = forced >= 0 ? forced : (kv_head_bytes > 64.0 * (1 << 20) ? 0 : 1);
+    const K6Variant variant = k6_variant(g.padded_tokens, d);
     // The kernels re-balance registers between warpgroups with setmaxnreg;
     // that only works if the launch allocates the full 168 x 384 pool.
     auto check_regs = [](const void* fn) {
@@ -123,47 +148,25 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       if (fa.numRegs * attn2::kThreads < 2 * 128 * 208 + 128 * 88)
         throw CudaError("K6 compiled with too few registers for its setmaxnreg plan");
     };
-    auto prepare = [&](const void* fn, int smem, bool& done) {
-      if (done) return;
-      check_regs(fn);
-      RP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      done = true;
+    auto launch = [&](const void* fn, int smem, int grid, int threads, auto&& go) {
+      prepare_kernel(fn, smem, check_regs);
+      go(grid, threads, smem);
+      RP_LAUNCHED();
     };
-    // Per-row-unit parameters shared by db and alt (soft-mask fields zero
-    // unless soft_bits is set).
-    auto row_params = [&]() {
-      attn2::Params p{};
-      p.row_ptr = row_ptr;
-      p.col_idx = col_idx;
-      p.row_order = row_order;
-      p.n_rows = static_cast<int>(g.blocks_per_dim);
-      p.heads = q.heads;
-      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
-      p.out = static_cast<__nv_bfloat16*>(o.data);
-      p.out_tok_stride = o.token_stride;
-      p.out_head_stride = o.head_stride;
-      p.scale_log2 = scale * 1.4426950408889634f;
-      p.soft_bits = soft_bits;
-      p.soft_row_bytes = g.row_bytes;
-      p.soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
-                                                    static_cast<double>(scale))
-                               : 0.f;
-      return p;
-    };
-    // the soft mask's dense lists run on the row-pair kernel (rp: fastest on
-    // dense masks)
-    if (variant == 0 || variant == 2 || variant == 5 || variant == 6 || soft_bits) {
-      // union block lists of the row pairs (2p, 2p+1), LPT order
+    const float soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
+                                                            static_cast<double>(scale))
+                                       : 0.f;
+    if (variant == K6Variant::kRP) {
+      // union block lists of the row pairs (2p, 2p+1)
       const int n_rows = static_cast<int>(g.blocks_per_dim);
       const int n_pairs = (n_rows + 1) / 2;
       const size_t cap = static_cast<size_t>(n_pairs) * n_rows;
-      int32_t *pcnt = nullptr, *prow = nullptr, *pcol = nullptr, *pord = nullptr;
+      int32_t *pcnt = nullptr, *prow = nullptr, *pcol = nullptr;
       uint8_t* pflag = nullptr;
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcnt), sizeof(int32_t) * (n_pairs + 1), stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prow), sizeof(int32_t) * (n_pairs + 1), stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcol), sizeof(int32_t) * cap, stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pflag), cap, stream));
-      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pord), sizeof(int32_t) * n_pairs, stream));
       const unsigned pg = static_cast<unsigned>((n_pairs + 127) / 128);
       attn3::pair_count_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, pcnt);
       RP_LAUNCHED();
@@ -172,17 +175,12 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       attn3::pair_fill_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, prow,
                                                      pcol, pflag);
       RP_LAUNCHED();
-      if (use_lpt_order()) {
-        csr::order_kernel<<<static_cast<unsigned>((n_pairs + 255) / 256), 256, 0, stream>>>(
-            pcnt, n_pairs, pord);
-        RP_LAUNCHED();
-      }
       attn3::Params p;
       p.row_ptr = row_ptr;
       p.prow_ptr = prow;
       p.pcol = pcol;
       p.pflag = pflag;
-      p.porder = use_lpt_order() ? pord : nullptr;
+      p.porder = nullptr;
       p.n_rows = n_rows;
       p.n_pairs = n_pairs;
       p.heads = q.heads;
@@ -194,130 +192,72 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.col_idx = col_idx;
       p.soft_bits = soft_bits;
       p.soft_row_bytes = g.row_bytes;
-      p.soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
-                                                    static_cast<double>(scale))
-                               : 0.f;
+      p.soft_delta = soft_delta;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-      if (variant == 6 && d == 128 && !soft_bits) {
-        // "mc": db per CTA, CTA pairs share their common K/V tiles by TMA
-        // multicast (attn_sm100_mc.cu)
-        static bool done = false;
-        const int smem = attn8::Layout<128>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn8::bsfa_fwd_mc_kernel<128>), smem, done);
-        const int clusters =
-            static_cast<int>(std::min<long long>(p.n_units, std::max(1, sm_count() / 2)));
-        attn8::bsfa_fwd_mc_kernel<128><<<2 * clusters, attn8::kThreads, smem, stream>>>(mq, mk,
-                                                                                     mv, p);
-      } else if (variant == 5 && d == 128 && !soft_bits) {
-        // "cta2": CTA pairs with M = 256 tcgen05 MMAs (attn_sm100_2cta.cu)
-        static bool done = false;
-        const int smem = attn7::Layout::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn7::bsfa_fwd_2cta_kernel), smem, done);
-        const CUtensorMap mk64 = make_map_bf16(k, 64);
-        const int clusters =
-            static_cast<int>(std::min<long long>(p.n_units, std::max(1, sm_count() / 2)));
-        attn7::bsfa_fwd_2cta_kernel<<<2 * clusters, attn7::kThreads, smem, stream>>>(mq, mk64,
-                                                                                    mv, p);
-      } else if (variant == 2 && !soft_bits) {
-        if (d == 128) {
-          static bool done = false;
-          const int smem = attn4::Layout<128>::kSmemBytes;
-          prepare(reinterpret_cast<const void*>(attn4::bsfa_fwd_rp2_kernel<128>), smem, done);
-          attn4::bsfa_fwd_rp2_kernel<128><<<grid, attn4::kThreads, smem, stream>>>(mq, mk, mv, p);
-        } else {
-          static bool done = false;
-          const int smem = attn4::Layout<64>::kSmemBytes;
-          prepare(reinterpret_cast<const void*>(attn4::bsfa_fwd_rp2_kernel<64>), smem, done);
-          attn4::bsfa_fwd_rp2_kernel<64><<<grid, attn4::kThreads, smem, stream>>>(mq, mk, mv, p);
-        }
-      } else if (soft_bits) {
-        if (d == 128) {
-          static bool done = false;
-          const int smem = attn3::Layout<128>::kSmemBytes;
-          prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128, true>), smem, done);
-          attn3::bsfa_fwd_rp_kernel<128, true><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv,
-                                                                                       p);
-        } else {
-          static bool done = false;
-          const int smem = attn3::Layout<64>::kSmemBytes;
-          prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<64, true>), smem, done);
-          attn3::bsfa_fwd_rp_kernel<64, true><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv,
-                                                                                      p);
-        }
-      } else if (d == 128) {
-        static bool done = false;
-        const int smem = attn3::Layout<128>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128>), smem, done);
-        attn3::bsfa_fwd_rp_kernel<128><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv, p);
+      auto rp_launch = [&](const void* fn, int smem, auto kern) {
+        launch(fn, smem, grid, attn3::kThreads, [&](int gr, int th, int sm) {
+          kern<<<gr, th, sm, stream>>>(mq, mk, mv, p);
+        });
+      };
+      if (d == 128) {
+        if (soft_bits)
+          rp_launch(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128, true>),
+                    attn3::Layout<128>::kSmemBytes, attn3::bsfa_fwd_rp_kernel<128, true>);
+        else
+          rp_launch(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<128>),
+                    attn3::Layout<128>::kSmemBytes, attn3::bsfa_fwd_rp_kernel<128>);
       } else {
-        static bool done = false;
-        const int smem = attn3::Layout<64>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<64>), smem, done);
-        attn3::bsfa_fwd_rp_kernel<64><<<grid, attn3::kThreads, smem, stream>>>(mq, mk, mv, p);
+        if (soft_bits)
+          rp_launch(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<64, true>),
+                    attn3::Layout<64>::kSmemBytes, attn3::bsfa_fwd_rp_kernel<64, true>);
+        else
+          rp_launch(reinterpret_cast<const void*>(attn3::bsfa_fwd_rp_kernel<64>),
+                    attn3::Layout<64>::kSmemBytes, attn3::bsfa_fwd_rp_kernel<64>);
       }
-      RP_LAUNCHED();
+      if (err_flag) {  // rp zero-fills empty rows without flagging them
+        csr::empty_row_flag_kernel<<<static_cast<unsigned>((g.blocks_per_dim + 255) / 256), 256,
+                                     0, stream>>>(row_ptr, g.blocks_per_dim, err_flag);
+        RP_LAUNCHED();
+      }
       for (void* ptr : {static_cast<void*>(pcnt), static_cast<void*>(prow),
-                        static_cast<void*>(pcol), static_cast<void*>(pflag),
-                        static_cast<void*>(pord)})
+                        static_cast<void*>(pcol), static_cast<void*>(pflag)})
         RP_CUDA(cudaFreeAsync(ptr, stream));
       return;
     }
-    if (variant == 3 && !soft_bits) {
-      // "alt": KV steps alternate between two softmax groups with separate
-      // accumulators (attn_sm100_alt.cu)
-      const attn2::Params p = row_params();
-      const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
-      if (d == 128) {
-        static bool done = false;
-        const int smem = attn5::Layout<128>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn5::bsfa_fwd_alt_kernel<128>), smem, done);
-        attn5::bsfa_fwd_alt_kernel<128><<<grid, attn5::kThreads, smem, stream>>>(mq, mk, mv, p);
-      } else {
-        static bool done = false;
-        const int smem = attn5::Layout<64>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn5::bsfa_fwd_alt_kernel<64>), smem, done);
-        attn5::bsfa_fwd_alt_kernel<64><<<grid, attn5::kThreads, smem, stream>>>(mq, mk, mv, p);
-      }
-      RP_LAUNCHED();
-      return;
-    }
     {
-      attn2::Params p = row_params();
-      // Exchange-free rescale protocol (DYNRAD_DB_LAG=1; off by default): a
-      // per-head max |k| pre-pass (one read of K) lets units skip the
-      // per-step exchange.  Single launches gain ~3.5 points, but under
-      // sustained back-to-back load (bench.py, tools/ab_k6.py: mean of 20)
-      // it measured ~2 % slower (the pre-pass plus the power-capped clock),
-      // so the default keeps the exchange.
-      static const bool lag_on = [] {
-        const char* e = std::getenv("DYNRAD_DB_LAG");
-        return e && std::strcmp(e, "1") == 0;
-      }();
-      float* kmax = nullptr;
-      if (lag_on && k.head_dim % 8 == 0) {
-        RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kmax), sizeof(float) * k.heads, stream));
-        RP_CUDA(cudaMemsetAsync(kmax, 0, sizeof(float) * k.heads, stream));
-        const long long n = k.tokens * k.heads;
-        attn2::kmax_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(k.data), k.tokens, k.heads, k.head_dim,
-            k.token_stride, k.head_stride, kmax);
-        RP_LAUNCHED();
-        p.kmax_head = kmax;
-      }
+      // "db": one query tile per CTA, score tile double-buffered in TMEM
+      attn2::Params p{};
+      p.row_ptr = row_ptr;
+      p.col_idx = col_idx;
+      p.row_order = use_lpt_order() ? row_order : nullptr;
+      p.n_rows = static_cast<int>(g.blocks_per_dim);
+      p.heads = q.heads;
+      p.n_units = static_cast<long long>(q.heads) * p.n_rows;
+      p.out = static_cast<__nv_bfloat16*>(o.data);
+      p.out_tok_stride = o.token_stride;
+      p.out_head_stride = o.head_stride;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      p.soft_bits = soft_bits;
+      p.soft_row_bytes = g.row_bytes;
+      p.soft_delta = soft_delta;
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
       if (d == 128) {
-        static bool done = false;
-        const int smem = attn2::Layout<128>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<128>), smem, done);
-        attn2::bsfa_fwd_db_kernel<128><<<grid, attn2::kThreads, smem, stream>>>(mq, mk, mv, p);
+        launch(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<128>),
+               attn2::Layout<128>::kSmemBytes, grid, attn2::kThreads, [&](int gr, int th, int sm) {
+                 attn2::bsfa_fwd_db_kernel<128><<<gr, th, sm, stream>>>(mq, mk, mv, p);
+               });
       } else {
-        static bool done = false;
-        const int smem = attn2::Layout<64>::kSmemBytes;
-        prepare(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<64>), smem, done);
-        attn2::bsfa_fwd_db_kernel<64><<<grid, attn2::kThreads, smem, stream>>>(mq, mk, mv, p);
+        launch(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<64>),
+               attn2::Layout<64>::kSmemBytes, grid, attn2::kThreads, [&](int gr, int th, int sm) {
+                 attn2::bsfa_fwd_db_kernel<64><<<gr, th, sm, stream>>>(mq, mk, mv, p);
+               });
       }
-      RP_LAUNCHED();
-      if (kmax) RP_CUDA(cudaFreeAsync(kmax, stream));
+      if (err_flag) {
+        // db zero-fills empty rows without flagging them: flag from the CSR
+        csr::empty_row_flag_kernel<<<static_cast<unsigned>((g.blocks_per_dim + 255) / 256), 256,
+                                     0, stream>>>(row_ptr, g.blocks_per_dim, err_flag);
+        RP_LAUNCHED();
+      }
       return;
     }
   } else {
@@ -381,25 +321,31 @@ struct HostStreams {
   cudaStream_t in = nullptr, out = nullptr;
 };
 HostStreams& host_streams() {
-  static HostStreams hs = [] {
-    HostStreams x;
+  // one pair per device (streams belong to the device current at creation)
+  static std::mutex mu;
+  static HostStreams per_dev[64];
+  int dev = 0;
+  RP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  HostStreams& x = per_dev[dev & 63];
+  if (!x.in) {
     RP_CUDA(cudaStreamCreateWithFlags(&x.in, cudaStreamNonBlocking));
     RP_CUDA(cudaStreamCreateWithFlags(&x.out, cudaStreamNonBlocking));
-    return x;
-  }();
-  return hs;
+  }
+  return x;
 }
 void keep_pool_memory() {
-  static bool done = [] {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~uint64_t{0};
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    return true;
-  }();
-  (void)done;
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  const uint64_t bit = uint64_t{1} << (dev & 63);
+  if (done.load() & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~uint64_t{0};
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(bit);
 }
 // Head chunks of the host-buffer pipeline (DYNRAD_E2E_CHUNKS, default 8:
 // measured 54.0 ms at 4 chunks, 47.5 ms at 8 for the Wan layer).
@@ -424,6 +370,10 @@ int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
 #ifdef RP_TRACE
 int rp_debug_trace(void* host) {
   return cudaMemcpyFromSymbol(host, attn2::g_trace, sizeof(attn2::g_trace)) == cudaSuccess ? 0 : 1;
+}
+int rp_debug_trace_pp(void* host) {
+  return cudaMemcpyFromSymbol(host, attn9::g_trace_pp, sizeof(attn9::g_trace_pp)) == cudaSuccess
+             ? 0 : 1;
 }
 #endif
 
@@ -480,29 +430,86 @@ rp_status rp_frame_pair_info(const rp_grid* g, const rp_config* c, int i, int j,
   });
 }
 
+static void sparse_attention_entry(const rp_grid* g, const rp_tensor* q, const rp_tensor* k,
+                                   const rp_tensor* v, rp_tensor* o, const int32_t* row_ptr,
+                                   const int32_t* col_idx, const int32_t* row_order,
+                                   float softmax_scale, int* err_flag, rp_stream stream) {
+  require_device();
+  check_grid(g);
+  check_tensor(q, "q");
+  check_tensor(k, "k");
+  check_tensor(v, "v");
+  check_tensor(o, "o");
+  if (k->tokens != q->tokens || v->tokens != q->tokens || k->heads != q->heads ||
+      v->heads != q->heads || k->head_dim != q->head_dim || v->head_dim != q->head_dim ||
+      k->dtype != q->dtype || v->dtype != q->dtype || o->dtype != q->dtype)
+    throw std::invalid_argument("feature batch: queries/keys/values shape mismatch");
+  if (g->padded_tokens < q->tokens)
+    throw std::invalid_argument("masked attention: mask smaller than batch");
+  if (o->tokens < g->padded_tokens || o->heads != q->heads || o->head_dim != q->head_dim)
+    throw std::invalid_argument("masked attention: output must be [S', heads, head_dim]");
+  if (!row_ptr || !col_idx) throw std::invalid_argument("masked attention: null row lists");
+  launch_attention(*g, *q, *k, *v, *o, row_ptr, col_idx, row_order, softmax_scale,
+                   reinterpret_cast<cudaStream_t>(stream), err_flag);
+}
+
 rp_status rp_sparse_attention_fwd(const rp_grid* g, const rp_tensor* q, const rp_tensor* k,
                                   const rp_tensor* v, rp_tensor* o, const int32_t* row_ptr,
                                   const int32_t* col_idx, const int32_t* row_order,
                                   float softmax_scale, rp_stream stream) {
   return guarded([&] {
-    require_device();
-    check_grid(g);
-    check_tensor(q, "q");
-    check_tensor(k, "k");
-    check_tensor(v, "v");
-    check_tensor(o, "o");
-    if (k->tokens != q->tokens || v->tokens != q->tokens || k->heads != q->heads ||
-        v->heads != q->heads || k->head_dim != q->head_dim || v->head_dim != q->head_dim ||
-        k->dtype != q->dtype || v->dtype != q->dtype || o->dtype != q->dtype)
-      throw std::invalid_argument("feature batch: queries/keys/values shape mismatch");
-    if (g->padded_tokens < q->tokens)
-      throw std::invalid_argument("masked attention: mask smaller than batch");
-    if (o->tokens < g->padded_tokens || o->heads != q->heads || o->head_dim != q->head_dim)
-      throw std::invalid_argument("masked attention: output must be [S', heads, head_dim]");
-    if (!row_ptr || !col_idx) throw std::invalid_argument("masked attention: null row lists");
-    launch_attention(*g, *q, *k, *v, *o, row_ptr, col_idx, row_order, softmax_scale,
-                     reinterpret_cast<cudaStream_t>(stream), nullptr);
+    sparse_attention_entry(g, q, k, v, o, row_ptr, col_idx, row_order, softmax_scale, nullptr,
+                           stream);
   });
+}
+
+rp_status rp_sparse_attention_fwd_checked(const rp_grid* g, const rp_tensor* q,
+                                          const rp_tensor* k, const rp_tensor* v, rp_tensor* o,
+                                          const int32_t* row_ptr, const int32_t* col_idx,
+                                          const int32_t* row_order, float softmax_scale,
+                                          int* err_flag_dev, rp_stream stream) {
+  return guarded([&] {
+    sparse_attention_entry(g, q, k, v, o, row_ptr, col_idx, row_order, softmax_scale,
+                           err_flag_dev, stream);
+  });
+}
+
+rp_status rp_random_batch(int64_t tokens, int heads, int head_dim, uint64_t seed,
+                          int first_head, rp_tensor* q, rp_tensor* k, rp_tensor* v,
+                          rp_stream stream) {
+  return guarded([&] {
+    require_device();
+    if (tokens < 1 || heads < 1 || head_dim < 1)
+      throw std::invalid_argument("feature batch: empty dimensions");
+    if (head_dim % 8) throw std::invalid_argument("random_batch: head_dim must be a multiple of 8");
+    if (first_head < 0) throw std::invalid_argument("random_batch: first_head must be >= 0");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    rp_tensor* dst[3] = {q, k, v};
+    for (int role = 1; role <= 3; ++role) {
+      rp_tensor* t = dst[role - 1];
+      if (!t) continue;
+      if (!t->data || t->tokens < tokens || t->heads < heads || t->head_dim != head_dim ||
+          (t->dtype != RP_F32 && t->dtype != RP_BF16) || t->token_stride % 8 ||
+          t->head_stride % 8)
+        throw std::invalid_argument("random_batch: output tensor shape / dtype / stride");
+      const int64_t n = tokens * heads * (head_dim / 8);
+      const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+      if (t->dtype == RP_BF16)
+        feat::random_batch_kernel<true><<<grid, 256, 0, s>>>(
+            tokens, heads, head_dim, seed, static_cast<uint64_t>(role), first_head, t->data,
+            t->token_stride, t->head_stride);
+      else
+        feat::random_batch_kernel<false><<<grid, 256, 0, s>>>(
+            tokens, heads, head_dim, seed, static_cast<uint64_t>(role), first_head, t->data,
+            t->token_stride, t->head_stride);
+      RP_LAUNCHED();
+    }
+  });
+}
+
+const char* rp_attention_kernel(const rp_grid* g, int dtype, int head_dim) {
+  if (dtype != RP_BF16) return "attn_f32_kernel";
+  return k6_kernel_name(g ? g->padded_tokens : 0, head_dim);
 }
 
 rp_status rp_mask_to_csr(const rp_grid* g, const uint8_t* bits, int32_t* row_ptr,
@@ -735,22 +742,6 @@ rp_status rp_soft_attention_fwd(const rp_grid* g, const rp_tensor* q, const rp_t
                      mask_bits_dev, epsilon);
     RP_CUDA(cudaFreeAsync(rp_, s));
     RP_CUDA(cudaFreeAsync(ci, s));
-  });
-}
-
-// Test support (not in the public header): run the UMMA descriptor probe.
-rp_status rp_debug_umma_probe(const void* A, const void* B, const void* P, const void* V,
-                              float* C1, float* C2, rp_stream stream) {
-  return guarded([&] {
-    require_device();
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int smem = 3 * 32768 + 1024;
-    RP_CUDA(cudaFuncSetAttribute(attn::umma_probe_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attn::umma_probe_kernel<<<1, 128, smem, s>>>(
-        static_cast<const __nv_bfloat16*>(A), static_cast<const __nv_bfloat16*>(B),
-        static_cast<const __nv_bfloat16*>(P), static_cast<const __nv_bfloat16*>(V), C1, C2);
-    RP_LAUNCHED();
   });
 }
 

@@ -146,5 +146,13 @@ __global__ void dense_lists_kernel(int64_t n, int32_t* __restrict__ row_ptr,
   if (i < n * n) col_idx[i] = static_cast<int32_t>(i % n);
 }
 
+// Flags a row without any active block (the reference's domain_error,
+// attention.cpp:85-86) for kernels that zero-fill such rows silently.
+__global__ void empty_row_flag_kernel(const int32_t* __restrict__ row_ptr, int64_t n,
+                                      int* __restrict__ flag) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && row_ptr[i + 1] == row_ptr[i]) atomicOr(flag, 1);
+}
+
 }  // namespace csr
 }  // namespace rp

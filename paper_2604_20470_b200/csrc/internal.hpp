@@ -60,6 +60,11 @@ rp_status guarded(F&& f) {
   }
 }
 
+// Opt a kernel into `smem` bytes of dynamic shared memory on the current
+// device (a per-(kernel, device) attribute: set once per device), after
+// running `check` (may be null) on it.
+void prepare_kernel(const void* fn, int smem, void (*check)(const void*) = nullptr);
+
 // Every compute entry point first checks that a CUDA device exists: the
 // product has no CPU fallback.
 void require_device();

@@ -24,6 +24,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -466,7 +467,21 @@ struct rp_plan_s {
   int64_t retained = 0, sampled = 0, scored = 0;
   FastEngine* fast = nullptr;
   int fast_heads = 0, fast_dim = 0;
-  ~rp_plan_s() { fast_engine_destroy(fast); }
+  // Builds of one plan may come from any stream: they are serialised on the
+  // host (mu) and on the device (each build's stream first waits for the
+  // previous build's completion event), because they share the cached masks
+  // and the fast engine's scratch buffers.  A plan belongs to the device of
+  // its first build.
+  std::mutex mu;
+  cudaEvent_t done_ev = nullptr;
+  int dev = -1;
+  ~rp_plan_s() {
+    if (done_ev) {
+      cudaEventSynchronize(done_ev);
+      cudaEventDestroy(done_ev);
+    }
+    fast_engine_destroy(fast);
+  }
 };
 
 namespace {
@@ -759,9 +774,7 @@ rp_status rp_plan_create(const rp_grid* g, const rp_config* c, uint64_t seed,
 }
 
 void rp_plan_destroy(rp_plan p) {
-  if (!p) return;
-  if (p->s) cudaStreamSynchronize(p->s);
-  delete p;
+  delete p;  // waits for the last build (done_ev) before freeing device state
 }
 
 rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
@@ -783,6 +796,20 @@ rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
       if (q->tokens < g.total_tokens || k->tokens < g.total_tokens)
         throw std::invalid_argument("build_mask: feature batch too short");
     }
+    std::lock_guard<std::mutex> lock(P->mu);
+    int dev = 0;
+    RP_CUDA(cudaGetDevice(&dev));
+    if (P->dev < 0) P->dev = dev;
+    if (P->dev != dev)
+      throw std::invalid_argument("build_mask: plan was created on another device");
+    if (P->done_ev) RP_CUDA(cudaStreamWaitEvent(s, P->done_ev, 0));
+    else RP_CUDA(cudaEventCreateWithFlags(&P->done_ev, cudaEventDisableTiming));
+    // whatever happens below, later builds order after this one's work
+    struct Record {
+      rp_plan_s* P;
+      cudaStream_t s;
+      ~Record() { cudaEventRecord(P->done_ev, s); }
+    } record{P, s};
     if (!P->d_jobs.p) {
       P->s = s;
       P->d_jobs = DevBuf<DJob>(std::max<size_t>(P->djobs.size(), 1), s, true);

@@ -833,20 +833,10 @@ static void launch_pass_cg(const CUtensorMap& mq, const CUtensorMap& mk, const S
   const int smem = SLayout<NC>::kSmemBytes;
   const int threads = Epi<CG>::kThreads;
   if (mode == 0) {
-    static bool attr = false;
-    if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 0, CG>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
+    prepare_kernel(reinterpret_cast<const void*>(score_kernel<NC, 0, CG>), smem);
     score_kernel<NC, 0, CG><<<grid, threads, smem, s>>>(mq, mk, p);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(score_kernel<NC, 1, CG>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
+    prepare_kernel(reinterpret_cast<const void*>(score_kernel<NC, 1, CG>), smem);
     score_kernel<NC, 1, CG><<<grid, threads, smem, s>>>(mq, mk, p);
   }
   RP_LAUNCHED();

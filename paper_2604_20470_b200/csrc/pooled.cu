@@ -359,12 +359,7 @@ rp_status rp_pooled_select(const rp_grid* g, const rp_config* c, const rp_tensor
         q->token_stride, q->head_stride, n_score_heads, q->head_dim, g->total_tokens,
         g->block_size, d_qp, d_kp);
     RP_LAUNCHED();
-    static bool attr = false;
-    if (!attr) {
-      RP_CUDA(cudaFuncSetAttribute(pooled::select_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    prepare_kernel(reinterpret_cast<const void*>(pooled::select_kernel), 200 * 1024);
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(q->head_dim)) /
                                            n_score_heads);
     const unsigned tiles = static_cast<unsigned>((nb + pooled::kT - 1) / pooled::kT);

@@ -464,10 +464,19 @@ def _tensor(t, dtype_code=None) -> L.Tensor:
                     t.stride(1))
 
 
-def _stream(stream=None):
+def _stream(stream=None, device=None):
+    """The stream a call is enqueued on: `stream`, else the current stream of
+    `device` (the inputs' device), else of the current device."""
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return C.c_void_p(s.cuda_stream)
+
+
+def _on(device):
+    """Make `device` current for a library call: the C ABI works on the
+    current CUDA device (kernel attributes, SM count, host-copy streams)."""
+    torch = _torch()
+    return torch.cuda.device(device if device is not None else torch.cuda.current_device())
 
 
 @dataclass
@@ -513,17 +522,21 @@ class Plan:
         """Returns the bit-packed mask as a uint8 CUDA tensor [S_b, row_bytes]."""
         torch = _torch()
         g = self.grid
+        dev = q.device if q is not None else (out.device if out is not None else None)
         if out is None:
-            out = torch.empty((g.blocks_per_dim, g.row_bytes), dtype=torch.uint8, device="cuda")
+            out = torch.empty((g.blocks_per_dim, g.row_bytes), dtype=torch.uint8,
+                              device=dev if dev is not None else "cuda")
+        dev = out.device
         tq = C.byref(_tensor(q)) if q is not None else None
         tk = C.byref(_tensor(k)) if k is not None else None
         if q is not None and n_score_heads <= 0:
             n_score_heads = q.shape[1]
         st = L.BuildStats()
-        L.check(L.lib().rp_plan_build_mask(self._h, tq, tk, int(n_score_heads),
-                                           C.c_void_p(out.data_ptr()),
-                                           C.byref(st) if stats is not None else None,
-                                           _stream(stream)))
+        with _on(dev):
+            L.check(L.lib().rp_plan_build_mask(self._h, tq, tk, int(n_score_heads),
+                                               C.c_void_p(out.data_ptr()),
+                                               C.byref(st) if stats is not None else None,
+                                               _stream(stream, dev)))
         if stats is not None:
             for name, _ in L.BuildStats._fields_:
                 stats[name] = getattr(st, name)
@@ -551,6 +564,28 @@ class FeatureBatch:
         return self.queries.shape[2]
 
 
+def random_batch(tokens: int, heads: int, head_dim: int, seed: int, with_values: bool = True,
+                 dtype="bf16", first_head: int = 0, device=None, stream=None) -> FeatureBatch:
+    """attention.hpp:62-63 random_batch, generated on the GPU: heads
+    [first_head, first_head + heads) of the reference's counter-based batch as
+    [tokens, heads, head_dim] tensors (bf16 = round-to-nearest-even of the
+    reference's float values, or float32)."""
+    torch = _torch()
+    tdt = torch.bfloat16 if dtype in ("bf16", torch.bfloat16) else torch.float32
+    dev = torch.device(device) if device is not None else torch.device("cuda",
+                                                                       torch.cuda.current_device())
+    ts = [torch.empty((tokens, heads, head_dim), dtype=tdt, device=dev)
+          for _ in range(3 if with_values else 2)]
+    descs = [_tensor(t) for t in ts]
+    with _on(dev):
+        L.check(L.lib().rp_random_batch(int(tokens), int(heads), int(head_dim),
+                                        C.c_uint64(seed & _M64), int(first_head),
+                                        C.byref(descs[0]), C.byref(descs[1]),
+                                        C.byref(descs[2]) if with_values else None,
+                                        _stream(stream, dev)))
+    return FeatureBatch(ts[0], ts[1], ts[2] if with_values else None)
+
+
 def build_mask(g: GridSpec, c: SparsityConfig, seed: int,
                options: Optional[BuildOptions] = None,
                features: Optional[FeatureBatch] = None,
@@ -572,20 +607,22 @@ def mask_to_csr(g: GridSpec, mask_dev, stream=None, out=None, trim: bool = True)
     torch = _torch()
     nb = g.blocks_per_dim
     cap = nb * nb
+    dev = mask_dev.device
     if out is None:
-        row_ptr = torch.empty(nb + 1, dtype=torch.int32, device="cuda")
-        col_idx = torch.empty(cap, dtype=torch.int32, device="cuda")
-        order = torch.empty(nb, dtype=torch.int32, device="cuda")
-        nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+        row_ptr = torch.empty(nb + 1, dtype=torch.int32, device=dev)
+        col_idx = torch.empty(cap, dtype=torch.int32, device=dev)
+        order = torch.empty(nb, dtype=torch.int32, device=dev)
+        nnz = torch.zeros(1, dtype=torch.int64, device=dev)
     else:
         row_ptr, col_idx, order, nnz = out
         cap = col_idx.numel()
     gc = g.c()
-    L.check(L.lib().rp_mask_to_csr(C.byref(gc), C.c_void_p(mask_dev.data_ptr()),
-                                   C.c_void_p(row_ptr.data_ptr()),
-                                   C.c_void_p(col_idx.data_ptr()), cap,
-                                   C.c_void_p(order.data_ptr()), C.c_void_p(nnz.data_ptr()),
-                                   _stream(stream)))
+    with _on(dev):
+        L.check(L.lib().rp_mask_to_csr(C.byref(gc), C.c_void_p(mask_dev.data_ptr()),
+                                       C.c_void_p(row_ptr.data_ptr()),
+                                       C.c_void_p(col_idx.data_ptr()), cap,
+                                       C.c_void_p(order.data_ptr()), C.c_void_p(nnz.data_ptr()),
+                                       _stream(stream, dev)))
     if not trim or out is not None:
         return row_ptr, col_idx, order
     n = int(nnz.item())
@@ -602,30 +639,51 @@ def mask_to_bsr(g: GridSpec, mask_dev, stream=None):
 
 
 def sparse_attention(g: GridSpec, q, k, v, row_ptr, col_idx, row_order=None, out=None,
-                     softmax_scale: float = 0.0, stream=None):
-    """Block-sparse attention forward on device tensors; out [S', heads, d]."""
+                     softmax_scale: float = 0.0, stream=None, check_empty: bool = False):
+    """Block-sparse attention forward on device tensors; out [S', heads, d].
+
+    A row without any active block is the reference's domain_error
+    (attention.cpp:85-86).  The device kernel zero-fills such rows; with
+    check_empty=True the kernel also raises a device flag, which this call
+    reads (synchronizing the stream) and turns into DomainError."""
     torch = _torch()
+    dev = q.device
     if out is None:
-        out = torch.empty((g.padded_tokens, q.shape[1], q.shape[2]), dtype=q.dtype,
-                          device=q.device)
+        out = torch.empty((g.padded_tokens, q.shape[1], q.shape[2]), dtype=q.dtype, device=dev)
     gc = g.c()
     tq, tk, tv, to = _tensor(q), _tensor(k), _tensor(v), _tensor(out)
-    L.check(L.lib().rp_sparse_attention_fwd(
-        C.byref(gc), C.byref(tq), C.byref(tk), C.byref(tv), C.byref(to),
-        C.c_void_p(row_ptr.data_ptr()), C.c_void_p(col_idx.data_ptr()),
-        C.c_void_p(row_order.data_ptr()) if row_order is not None else None,
-        C.c_float(softmax_scale), _stream(stream)))
+    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_empty else None
+    with _on(dev):
+        L.check(L.lib().rp_sparse_attention_fwd_checked(
+            C.byref(gc), C.byref(tq), C.byref(tk), C.byref(tv), C.byref(to),
+            C.c_void_p(row_ptr.data_ptr()), C.c_void_p(col_idx.data_ptr()),
+            C.c_void_p(row_order.data_ptr()) if row_order is not None else None,
+            C.c_float(softmax_scale), C.c_void_p(flag.data_ptr()) if flag is not None else None,
+            _stream(stream, dev)))
+    if flag is not None and int(flag.item()):
+        raise DomainError("masked attention: row has no active key")
     return out
+
+
+def attention_kernel(g: GridSpec, dtype="bf16", head_dim: int = 128) -> str:
+    """Name of the stage-(d) kernel the library launches for this grid, dtype
+    and head_dim (bf16: db, or rp once one head's K + V exceed 64 MiB;
+    DYNRAD_K6 forces one)."""
+    code = L.RP_BF16 if dtype in ("bf16", L.RP_BF16) else L.RP_F32
+    gc = g.c()
+    return L.lib().rp_attention_kernel(C.byref(gc), code, int(head_dim)).decode()
 
 
 def expand_mask(mask_dev, g: GridSpec, stream=None):
     """mask.cpp:52-66 on device: token-level bits [S', ceil(S'/8)] uint8."""
     torch = _torch()
     trb = (g.padded_tokens + 7) // 8
-    out = torch.empty((g.padded_tokens, trb), dtype=torch.uint8, device="cuda")
+    dev = mask_dev.device
+    out = torch.empty((g.padded_tokens, trb), dtype=torch.uint8, device=dev)
     gc = g.c()
-    L.check(L.lib().rp_expand_mask(C.byref(gc), C.c_void_p(mask_dev.data_ptr()),
-                                   C.c_void_p(out.data_ptr()), _stream(stream)))
+    with _on(dev):
+        L.check(L.lib().rp_expand_mask(C.byref(gc), C.c_void_p(mask_dev.data_ptr()),
+                                       C.c_void_p(out.data_ptr()), _stream(stream, dev)))
     return out
 
 
@@ -640,10 +698,11 @@ def soft_attention(g: GridSpec, q, k, v, mask_dev, epsilon: float, out=None,
                           device=q.device)
     gc = g.c()
     tq, tk, tv, to = _tensor(q), _tensor(k), _tensor(v), _tensor(out)
-    L.check(L.lib().rp_soft_attention_fwd(
-        C.byref(gc), C.byref(tq), C.byref(tk), C.byref(tv), C.byref(to),
-        C.c_void_p(mask_dev.data_ptr()), C.c_double(epsilon), C.c_float(softmax_scale),
-        _stream(stream)))
+    with _on(q.device):
+        L.check(L.lib().rp_soft_attention_fwd(
+            C.byref(gc), C.byref(tq), C.byref(tk), C.byref(tv), C.byref(to),
+            C.c_void_p(mask_dev.data_ptr()), C.c_double(epsilon), C.c_float(softmax_scale),
+            _stream(stream, q.device)))
     return out
 
 

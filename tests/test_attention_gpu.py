@@ -46,23 +46,6 @@ def _torch_ref(q, k, v, dense, B, S):
     return out
 
 
-def test_umma_descriptor_probe(cuda):
-    """Pins the smem/TMEM operand conventions the tcgen05 kernels rely on."""
-    import ctypes as C
-    from paper_2604_20470_b200 import _lib
-    g = torch.Generator(device="cpu").manual_seed(0)
-    A, B, P, V = (torch.randn(128, 128, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
-    C1 = torch.zeros(128, 128, device="cuda")
-    C2 = torch.zeros(128, 128, device="cuda")
-    _lib.check(_lib.lib().rp_debug_umma_probe(*(C.c_void_p(t.data_ptr()) for t in (A, B, P, V, C1, C2)),
-                                              C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-    torch.cuda.synchronize()
-    e1 = A.float() @ B.float().T
-    e2 = P.float() @ V.float()
-    assert torch.allclose(C1, e1, rtol=1e-3, atol=1e-2), (C1 - e1).abs().max()
-    assert torch.allclose(C2, e2, rtol=1e-3, atol=1e-2), (C2 - e2).abs().max()
-
-
 @pytest.mark.parametrize("nf,nt,heads,d,density", [
     (4, 300, 3, 128, 0.5),   # padded last block, odd heads (single-tile unit)
     (4, 300, 2, 64, 0.4),
@@ -185,6 +168,12 @@ def test_empty_row_gives_zeros_on_device(cuda):
     keep = torch.ones(512, dtype=torch.bool, device="cuda")
     keep[256:384] = False
     assert rel_rows(out[keep].cpu().numpy(), ref[keep].cpu().numpy()) < 2e-2
+    # the checked entry point surfaces the reference's domain_error
+    with pytest.raises(rp.DomainError):
+        rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, check_empty=True)
+    full = pyoracle.pack_dense(np.eye(4, dtype=np.uint8))
+    rpf, cif, orf = rp.mask_to_csr(g, torch.from_numpy(full).cuda())
+    rp.sparse_attention(g, q, k, v, rpf, cif, orf, check_empty=True)  # no error
 
 
 def test_host_pipeline_matches_device_path(cuda):

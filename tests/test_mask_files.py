@@ -60,3 +60,21 @@ def test_files_byte_identical_to_reference_writer(tmp_path, ref, fmt):
     if fmt == 0:
         dim, bits = ref.read_mask(str(ours))
         assert dim == m.dim and np.array_equal(bits, m.bits)
+
+
+def test_production_goldens_are_consistent():
+    """The production-scale dynamic goldens (reference build_mask output,
+    tests/golden/make_golden_production.py) parse as DRBM and carry the
+    active-block counts recorded with them."""
+    import json
+    import os
+
+    from golden_util import GOLDEN, read_drbm
+    with open(os.path.join(GOLDEN, "production_meta.json")) as f:
+        meta = json.load(f)
+    for name, m in meta.items():
+        dim, bits = read_drbm(os.path.join(GOLDEN, f"{name}_mid.drbm"))
+        nb = (m["nf"] * m["nt"] + m["bs"] - 1) // m["bs"]
+        assert dim == nb
+        assert int(np.unpackbits(bits, axis=1, bitorder="little")[:, :dim].sum()) == m["nnz"]
+    assert meta["hunyuan"]["nnz"] == 567038

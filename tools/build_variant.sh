@@ -11,4 +11,4 @@ mkdir -p $ROOT/variants $B/var
 nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
   -I$ROOT/include -I$C --expt-relaxed-constexpr -Xptxas -v $2 -c -o $B/var/$1.o $C/capi.cu 2> $B/var/$1.log
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/variants/$1.so $B/var/$1.o $(ls $B/*.o | grep -v "/capi.o")
-grep -A1 "bsfa_fwd_kernelILi128" $B/var/$1.log | grep -o "Used [0-9]* registers.*" | head -1
+grep -A1 "pp_kernelILi128" $B/var/$1.log | grep -o "Used [0-9]* registers.*" | head -1
