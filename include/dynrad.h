@@ -315,6 +315,21 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g,
                                          int head_dim, void* o_host,
                                          rp_stream stream);
 
+/* One whole attention layer from host buffers, stages (a)-(d): host Q/K/V
+ * [tokens, heads, d] (pinned for full PCIe speed; f32 or bf16) are copied in
+ * by head chunks; the plan builds the block mask (rp_plan_build_mask; in
+ * dynamic mode from the first n_score_heads heads of Q/K, in static mode
+ * from its cache, n_score_heads may be 0), then the row lists, and every
+ * chunk's attention runs as soon as its inputs have landed while finished
+ * chunks are copied out.  o_host: [S', heads, d]; mask_bits_host_out (may
+ * be NULL) receives the bit-packed mask.  Synchronous.  RP_DOMAIN_ERROR
+ * when a row has no active block (attention.cpp:85-86; the output is still
+ * written, with zeros in that row). */
+rp_status rp_sparse_layer_host(rp_plan plan, const rp_grid* g, const void* q_host,
+                               const void* k_host, const void* v_host, int dtype,
+                               int64_t tokens, int heads, int head_dim, int n_score_heads,
+                               void* o_host, uint8_t* mask_bits_host_out, rp_stream stream);
+
 /* Stage (b) of rp_pooled_select on its own: block means of the first n_heads
  * heads of x (bf16 [tokens, heads, d]) -> out_dev [S_b, n_heads * d] f32.
  * One pass over S * n_heads * d bf16 (HBM-bound; the bench's roofline for
@@ -402,6 +417,18 @@ rp_status rp_objective(const rp_proxy_cache* cache, const rp_config* c,
 /* Number of CUDA kernels this library has launched in the calling process
  * (all entry points); used by bench.py to report gpu_launches. */
 int64_t rp_kernel_launch_count(void);
+
+/* Per-stage device timing (measurement support for bench.py).  While
+ * enabled, the entry points record CUDA events on their launching stream
+ * around each stage; rp_profile_read waits for them and returns, per stage
+ * index, the summed milliseconds and the number of occurrences.  Stages:
+ * 0 mask prep (base copy, norms), 1 tensor-core scoring pass 1 (stats),
+ * 2 per-frame-pair thresholds, 3 tensor-core scoring pass 2 (select),
+ * 4 exact recheck + fallback, 5 theta_c / theta_m apply, 6 CSR,
+ * 7 stage-(d) attention, 8 exact fp64 scoring engine, 9 static build.
+ * rp_profile_stages(1) clears previous records. */
+void rp_profile_stages(int enable);
+rp_status rp_profile_read(double* total_ms, int64_t* count, int n_stages);
 
 #ifdef __cplusplus
 }

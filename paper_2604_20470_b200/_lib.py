@@ -155,6 +155,10 @@ _SIGS = {
                                  _v, _v, C.c_float, _v], C.c_int),
     "rp_sparse_attention_fwd_checked": ([_P(Grid), _P(Tensor), _P(Tensor), _P(Tensor),
                                          _P(Tensor), _v, _v, _v, C.c_float, _v, _v], C.c_int),
+    "rp_sparse_layer_host": ([_v, _P(Grid), _v, _v, _v, C.c_int, C.c_int64, C.c_int, C.c_int,
+                              C.c_int, _v, _v, _v], C.c_int),
+    "rp_profile_stages": ([C.c_int], None),
+    "rp_profile_read": ([_v, _v, C.c_int], C.c_int),
     "rp_attention_kernel": ([_P(Grid), C.c_int, C.c_int], C.c_char_p),
     "rp_random_batch": ([C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, _P(Tensor),
                          _P(Tensor), _P(Tensor), _v], C.c_int),

@@ -26,6 +26,41 @@
 namespace rp {
 
 static thread_local std::string t_err;
+
+// ----------------------------------------------------- stage profiling --
+namespace {
+struct StageRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<StageRec> g_prof_recs;
+std::vector<std::pair<int, cudaEvent_t>> g_prof_open;
+}  // namespace
+bool profiling_on() { return g_prof_on.load(std::memory_order_relaxed); }
+void stage_begin(int stage, cudaStream_t s) {
+  if (!profiling_on()) return;
+  cudaEvent_t e;
+  RP_CUDA(cudaEventCreate(&e));
+  RP_CUDA(cudaEventRecord(e, s));
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  g_prof_open.emplace_back(stage, e);
+}
+void stage_end(int stage, cudaStream_t s) {
+  if (!profiling_on()) return;
+  cudaEvent_t e;
+  RP_CUDA(cudaEventCreate(&e));
+  RP_CUDA(cudaEventRecord(e, s));
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  for (auto it = g_prof_open.rbegin(); it != g_prof_open.rend(); ++it)
+    if (it->first == stage) {
+      g_prof_recs.push_back({stage, it->second, e});
+      g_prof_open.erase(std::next(it).base());
+      return;
+    }
+  cudaEventDestroy(e);
+}
 std::atomic<long long> g_launches{0};
 void set_error(const std::string& msg) { t_err = msg; }
 
@@ -365,6 +400,36 @@ using namespace rp;
 extern "C" {
 
 const char* rp_last_error(void) { return t_err.c_str(); }
+
+void rp_profile_stages(int enable) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  for (auto& r : g_prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof_recs.clear();
+  for (auto& o : g_prof_open) cudaEventDestroy(o.second);
+  g_prof_open.clear();
+  g_prof_on.store(enable != 0);
+}
+
+rp_status rp_profile_read(double* total_ms, int64_t* count, int n) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    for (int i = 0; i < n; ++i) {
+      total_ms[i] = 0.0;
+      count[i] = 0;
+    }
+    for (auto& r : g_prof_recs) {
+      if (r.stage < 0 || r.stage >= n) continue;
+      RP_CUDA(cudaEventSynchronize(r.b));
+      float ms = 0.f;
+      RP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      total_ms[r.stage] += ms;
+      ++count[r.stage];
+    }
+  });
+}
 const char* rp_version(void) { return "dynrad-b200 0.1 (sm_100a)"; }
 int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
 #ifdef RP_TRACE
@@ -449,8 +514,10 @@ static void sparse_attention_entry(const rp_grid* g, const rp_tensor* q, const r
   if (o->tokens < g->padded_tokens || o->heads != q->heads || o->head_dim != q->head_dim)
     throw std::invalid_argument("masked attention: output must be [S', heads, head_dim]");
   if (!row_ptr || !col_idx) throw std::invalid_argument("masked attention: null row lists");
-  launch_attention(*g, *q, *k, *v, *o, row_ptr, col_idx, row_order, softmax_scale,
-                   reinterpret_cast<cudaStream_t>(stream), err_flag);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  stage_begin(kStageAttention, s);
+  launch_attention(*g, *q, *k, *v, *o, row_ptr, col_idx, row_order, softmax_scale, s, err_flag);
+  stage_end(kStageAttention, s);
 }
 
 rp_status rp_sparse_attention_fwd(const rp_grid* g, const rp_tensor* q, const rp_tensor* k,
@@ -522,7 +589,9 @@ rp_status rp_mask_to_csr(const rp_grid* g, const uint8_t* bits, int32_t* row_ptr
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int32_t* counts = nullptr;
     RP_CUDA(cudaMallocAsync(&counts, sizeof(int32_t) * (g->blocks_per_dim + 1), s));
+    stage_begin(kStageCsr, s);
     launch_csr(*g, bits, row_ptr, col_idx, col_cap, row_order, nnz, counts, s);
+    stage_end(kStageCsr, s);
     RP_CUDA(cudaFreeAsync(counts, s));
   });
 }
@@ -682,6 +751,146 @@ static void host_attention(const rp_grid* g, const uint8_t* mask_bits_host, cons
     cudaEventDestroy(start_ev);
 }
 
+static void rethrow(rp_status st) {
+  const std::string m = t_err;
+  switch (st) {
+    case RP_OK: return;
+    case RP_INVALID_ARGUMENT: throw std::invalid_argument(m);
+    case RP_OUT_OF_RANGE: throw std::out_of_range(m);
+    case RP_DOMAIN_ERROR: throw std::domain_error(m);
+    case RP_RUNTIME_ERROR: throw std::runtime_error(m);
+    default: throw CudaError(m);
+  }
+}
+
+// One attention layer from host buffers (rp_sparse_layer_host): Q/K/V are
+// copied in by head chunks over a dedicated H2D stream; the mask is built by
+// the plan from the first chunk (which holds the scoring heads) as soon as
+// it lands, row lists follow, and each chunk's attention runs as its inputs
+// arrive while the previous chunk's output is copied out on a D2H stream.
+static void layer_host(rp_plan plan, const rp_grid* g, const void* q_host, const void* k_host,
+                       const void* v_host, int dtype, int64_t tokens, int heads, int head_dim,
+                       int n_score_heads, void* o_host, uint8_t* mask_out, rp_stream stream) {
+  require_device();
+  check_grid(g);
+  if (!plan) throw std::invalid_argument("sparse layer: null plan");
+  if (tokens < 1 || heads < 1 || head_dim < 1)
+    throw std::invalid_argument("feature batch: empty dimensions");
+  if (g->padded_tokens < tokens)
+    throw std::invalid_argument("masked attention: mask smaller than batch");
+  if (n_score_heads < 0 || n_score_heads > heads)
+    throw std::invalid_argument("sparse layer: n_score_heads must be in [0, heads]");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t es = dtype == RP_BF16 ? 2 : 4;
+  const size_t row_in = static_cast<size_t>(heads) * head_dim * es;
+  const size_t in_bytes = static_cast<size_t>(tokens) * row_in;
+  const size_t out_bytes = static_cast<size_t>(g->padded_tokens) * row_in;
+  const size_t mask_bytes = static_cast<size_t>(g->blocks_per_dim * g->row_bytes);
+  const int64_t nb = g->blocks_per_dim;
+  keep_pool_memory();
+  uint8_t *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr, *dm = nullptr;
+  int32_t *rp_ = nullptr, *ci = nullptr, *cnt = nullptr;
+  int* flag = nullptr;
+  struct Free {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    ~Free() {
+      for (void* p : ptrs)
+        if (p) cudaFreeAsync(p, s);
+    }
+  } fr{s, {}};
+  auto alloc = [&](auto** p, size_t b) {
+    RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), b, s));
+    fr.ptrs.push_back(*p);
+  };
+  alloc(&dm, mask_bytes);
+  alloc(&rp_, sizeof(int32_t) * (nb + 1));
+  alloc(&ci, sizeof(int32_t) * nb * nb);
+  alloc(&cnt, sizeof(int32_t) * (nb + 1));
+  alloc(&flag, sizeof(int));
+  alloc(&dq, in_bytes);
+  alloc(&dk, in_bytes);
+  alloc(&dv, in_bytes);
+  alloc(&dout, out_bytes);
+  RP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  const int chunks = std::max(1, std::min(heads, e2e_chunks()));
+  const int per = std::max((heads + chunks - 1) / chunks, n_score_heads);
+  HostStreams& hs = host_streams();
+  std::vector<cudaEvent_t> evs;
+  auto event = [&]() {
+    cudaEvent_t e;
+    RP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    evs.push_back(e);
+    return e;
+  };
+  struct Destroy {
+    std::vector<cudaEvent_t>& v;
+    ~Destroy() {
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+    }
+  } destroy{evs};
+  cudaEvent_t start_ev = event();
+  RP_CUDA(cudaEventRecord(start_ev, s));  // allocations above are ordered on s
+  RP_CUDA(cudaStreamWaitEvent(hs.in, start_ev, 0));
+  const int64_t ts = static_cast<int64_t>(heads) * head_dim;
+  // Issue order per chunk: H2D(c), [c == 0: mask + row lists], attention(c),
+  // D2H(c) -- interleaved so both copy directions stay busy (queueing every
+  // H2D first measured 63 ms instead of 47 ms for the Wan layer).
+  int c = 0;
+  for (int h0 = 0; h0 < heads; h0 += per, ++c) {
+    const int hc = std::min(per, heads - h0);
+    const size_t off = static_cast<size_t>(h0) * head_dim * es;
+    const size_t w = static_cast<size_t>(hc) * head_dim * es;
+    for (auto pr : {std::make_pair(dq, q_host), std::make_pair(dk, k_host),
+                    std::make_pair(dv, v_host)})
+      RP_CUDA(cudaMemcpy2DAsync(pr.first + off, row_in, static_cast<const uint8_t*>(pr.second) + off,
+                                row_in, w, static_cast<size_t>(tokens), cudaMemcpyHostToDevice,
+                                hs.in));
+    cudaEvent_t in_done = event();
+    RP_CUDA(cudaEventRecord(in_done, hs.in));
+    RP_CUDA(cudaStreamWaitEvent(s, in_done, 0));
+    if (c == 0) {
+      // stages (a)-(c) from the first chunk (it holds the scoring heads)
+      rp_tensor tq{dq, dtype, tokens, hc, head_dim, ts, head_dim};
+      rp_tensor tk = tq;
+      tk.data = dk;
+      rethrow(rp_plan_build_mask(plan, n_score_heads ? &tq : nullptr,
+                                 n_score_heads ? &tk : nullptr, n_score_heads, dm, nullptr,
+                                 stream));
+      stage_begin(kStageCsr, s);
+      launch_csr(*g, dm, rp_, ci, nb * nb, nullptr, nullptr, cnt, s);
+      csr::empty_row_flag_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(
+          rp_, nb, flag);
+      RP_LAUNCHED();
+      stage_end(kStageCsr, s);
+      if (mask_out)
+        RP_CUDA(cudaMemcpyAsync(mask_out, dm, mask_bytes, cudaMemcpyDeviceToHost, s));
+    }
+    rp_tensor cq{dq + off, dtype, tokens, hc, head_dim, ts, head_dim};
+    rp_tensor ck = cq, cv = cq, co = cq;
+    ck.data = dk + off;
+    cv.data = dv + off;
+    co.data = dout + off;
+    co.tokens = g->padded_tokens;
+    stage_begin(kStageAttention, s);
+    launch_attention(*g, cq, ck, cv, co, rp_, ci, nullptr, 0.f, s, nullptr);
+    stage_end(kStageAttention, s);
+    cudaEvent_t k_done = event();
+    RP_CUDA(cudaEventRecord(k_done, s));
+    RP_CUDA(cudaStreamWaitEvent(hs.out, k_done, 0));
+    RP_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(o_host) + off, row_in, dout + off, row_in, w,
+                              static_cast<size_t>(g->padded_tokens), cudaMemcpyDeviceToHost,
+                              hs.out));
+  }
+  int hflag = 0;
+  cudaEvent_t out_done = event();
+  RP_CUDA(cudaEventRecord(out_done, hs.out));
+  RP_CUDA(cudaStreamWaitEvent(s, out_done, 0));
+  RP_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RP_CUDA(cudaStreamSynchronize(s));
+  if (hflag) throw std::domain_error("masked attention: row has no active key");
+}
+
 static void check_epsilon(double eps) {
   if (!(eps > 0.0)) throw std::invalid_argument("masked attention: epsilon must be positive");
 }
@@ -697,6 +906,16 @@ rp_status rp_masked_attention_exact_host(const rp_grid* g, const uint8_t* mask_b
   return guarded([&] {
     host_attention(g, mask_bits_host, q_host, k_host, v_host, dtype, tokens, heads, head_dim,
                    o_host, stream, false, 0.0);
+  });
+}
+
+rp_status rp_sparse_layer_host(rp_plan plan, const rp_grid* g, const void* q_host,
+                               const void* k_host, const void* v_host, int dtype, int64_t tokens,
+                               int heads, int head_dim, int n_score_heads, void* o_host,
+                               uint8_t* mask_bits_host_out, rp_stream stream) {
+  return guarded([&] {
+    layer_host(plan, g, q_host, k_host, v_host, dtype, tokens, heads, head_dim, n_score_heads,
+               o_host, mask_bits_host_out, stream);
   });
 }
 

@@ -65,6 +65,26 @@ rp_status guarded(F&& f) {
 // running `check` (may be null) on it.
 void prepare_kernel(const void* fn, int smem, void (*check)(const void*) = nullptr);
 
+// Optional per-stage CUDA-event timing (rp_profile_stages): when enabled,
+// library entry points bracket their kernels with events on the launching
+// stream; bench.py reads the per-stage device time of the timed region.
+enum Stage : int {
+  kStageMaskPrep = 0,    // base-mask copy, norms, per-tile max |k|
+  kStageScoreStats = 1,  // tensor-core scoring, pass 1 (per-pair mu / sigma)
+  kStageJobStats = 2,    // per-frame-pair thresholds
+  kStageScoreSelect = 3, // tensor-core scoring, pass 2 (keep / drop / undecided)
+  kStageRecheck = 4,     // exact fp64 re-score of undecided pairs + fallback
+  kStageApply = 5,       // theta_c / theta_m tile aggregation, mask copy-out
+  kStageCsr = 6,         // bitmask -> row lists
+  kStageAttention = 7,   // stage (d)
+  kStageExactScore = 8,  // exact fp64 scoring engine (all of a10-a12)
+  kStageStatic = 9,      // static Fisher-Yates build (first call of a plan)
+  kNumStages = 10
+};
+bool profiling_on();
+void stage_begin(int stage, cudaStream_t s);
+void stage_end(int stage, cudaStream_t s);
+
 // Every compute entry point first checks that a CUDA device exists: the
 // product has no CPU fallback.
 void require_device();

@@ -822,7 +822,9 @@ rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
       if (!P->static_ready) {
         P->cached = DevBuf<uint32_t>(P->words, s, true);
         RP_CUDA(cudaMemcpyAsync(P->cached.p, P->base.p, P->words * 4, cudaMemcpyDeviceToDevice, s));
+        stage_begin(kStageStatic, s);
         build_static(*P, P->cached.p, s);
+        stage_end(kStageStatic, s);
         P->static_ready = true;
       }
       RP_CUDA(cudaMemcpyAsync(mask_bits_dev, P->cached.p, bytes, cudaMemcpyDeviceToDevice, s));
@@ -857,7 +859,9 @@ rp_status rp_plan_build_mask(rp_plan P, const rp_tensor* q, const rp_tensor* k,
         rechecked = fr.rechecked;
         fallbacks = fr.fallbacks;
       } else {
+        stage_begin(kStageExactScore, s);
         build_dynamic_exact(*P, f, work.p, &rechecked, stats ? &fallbacks : nullptr, s);
+        stage_end(kStageExactScore, s);
       }
       RP_CUDA(cudaMemcpyAsync(mask_bits_dev, work.p, bytes, cudaMemcpyDeviceToDevice, s));
     }

@@ -877,6 +877,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   qv.heads = e->heads;
   kv.heads = e->heads;
   const CUtensorMap mq = make_map_bf16(qv), mk = make_map_bf16(kv);
+  stage_begin(kStageMaskPrep, s);
   RP_CUDA(cudaMemsetAsync(e->d_counts, 0, sizeof(uint32_t) * std::max<int64_t>(e->ncounts, 1), s));
   RP_CUDA(cudaMemsetAsync(e->d_kept, 0, sizeof(unsigned long long) * (nj + 1), s));
   RP_CUDA(cudaMemsetAsync(e->d_qn, 0, sizeof(float) * g.padded_tokens, s));
@@ -892,6 +893,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   tile_max_kernel<<<static_cast<unsigned>((ktiles + 7) / 8), 256, 0, s>>>(e->d_kn, g.total_tokens,
                                                                          ktiles, e->d_kmax);
   RP_LAUNCHED();
+  stage_end(kStageMaskPrep, s);
 
   SParams p{};
   p.jobs = e->d_jobs;
@@ -923,20 +925,26 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = std::min(p.n_units, sms);
   for (int mode = 0; mode < 2; ++mode) {
+    const int st = mode == 0 ? kStageScoreStats : kStageScoreSelect;
+    stage_begin(st, s);
     switch (e->nc) {
       case 1: launch_pass<1>(mq, mk, p, mode, grid, s); break;
       case 2: launch_pass<2>(mq, mk, p, mode, grid, s); break;
       case 3: launch_pass<3>(mq, mk, p, mode, grid, s); break;
       default: launch_pass<4>(mq, mk, p, mode, grid, s); break;
     }
+    stage_end(st, s);
     if (mode == 0) {
+      stage_begin(kStageJobStats, s);
       job_stats_kernel<<<(nj + 127) / 128, 128, 0, s>>>(e->d_item_stats, e->d_job_item_off, nj,
                                                        e->d_jobs, p.score_scale, delta_floor,
                                                        e->d_job_stats, e->d_job_thr);
       RP_LAUNCHED();
+      stage_end(kStageJobStats, s);
     }
   }
   // exact re-score of the pairs within their error bound of tau
+  stage_begin(kStageRecheck, s);
   {
     const int ew = 4 * score_cg(1);  // slots are written by the select pass
     const long long groups = static_cast<long long>(e->items.size()) * ew;
@@ -970,7 +978,9 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
       RP_CUDA(cudaFreeAsync(sc, s));
     }
   }
+  stage_end(kStageRecheck, s);
   // theta_c / theta_m per block tile of every scored frame pair
+  stage_begin(kStageApply, s);
   const int64_t chunk = int64_t{1} << 30;
   for (int64_t b = 0; b < static_cast<int64_t>(e->tiles.size()); b += chunk) {
     const int64_t n = std::min<int64_t>(chunk, e->tiles.size() - b);
@@ -981,6 +991,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
                                                          e->amin, 1);
     RP_LAUNCHED();
   }
+  stage_end(kStageApply, s);
 }
 
 }  // namespace mask

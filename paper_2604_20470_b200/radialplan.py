@@ -665,6 +665,52 @@ def sparse_attention(g: GridSpec, q, k, v, row_ptr, col_idx, row_order=None, out
     return out
 
 
+def sparse_layer_host(plan: "Plan", q, k, v, n_score_heads: int = 0, out=None, mask_out=None,
+                      stream=None):
+    """One attention layer (stages a-d) from host buffers through
+    rp_sparse_layer_host: q/k/v torch CPU tensors [tokens, heads, d]
+    (bf16 or float32; pin them for full PCIe speed).  Returns out
+    [S', heads, d] (host); mask_out (uint8 [S_b, row_bytes] host tensor)
+    receives the block mask when given."""
+    torch = _torch()
+    g = plan.grid
+    for t in (q, k, v):
+        if t.is_cuda or not t.is_contiguous() or t.shape != q.shape or t.dtype != q.dtype:
+            raise InvalidArgument("sparse layer: q/k/v must be contiguous host tensors of one shape")
+    code = {torch.float32: L.RP_F32, torch.bfloat16: L.RP_BF16}.get(q.dtype)
+    if code is None:
+        raise InvalidArgument("feature tensor dtype must be float32 or bfloat16")
+    tok, h, d = q.shape
+    if out is None:
+        out = torch.empty((g.padded_tokens, h, d), dtype=q.dtype, pin_memory=True)
+    gc = g.c()
+    L.check(L.lib().rp_sparse_layer_host(
+        plan._h, C.byref(gc), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
+        C.c_void_p(v.data_ptr()), code, tok, h, d, int(n_score_heads), C.c_void_p(out.data_ptr()),
+        C.c_void_p(mask_out.data_ptr()) if mask_out is not None else None,
+        _stream(stream)))
+    return out
+
+
+STAGES = ("mask_prep", "score_stats", "job_stats", "score_select", "recheck", "apply", "csr",
+          "attention", "exact_score", "static_build")
+
+
+def profile_stages(enable: bool) -> None:
+    """Start (clearing earlier records) or stop per-stage CUDA-event timing
+    inside the library (rp_profile_stages)."""
+    L.lib().rp_profile_stages(int(bool(enable)))
+
+
+def profile_read() -> dict:
+    """{stage: (total_ms, count)} of the events recorded since profile_stages(True)."""
+    n = len(STAGES)
+    tot = (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    L.check(L.lib().rp_profile_read(tot, cnt, n))
+    return {name: (tot[i], int(cnt[i])) for i, name in enumerate(STAGES) if cnt[i]}
+
+
 def attention_kernel(g: GridSpec, dtype="bf16", head_dim: int = 128) -> str:
     """Name of the stage-(d) kernel the library launches for this grid, dtype
     and head_dim (bf16: db, or rp once one head's K + V exceed 64 MiB;

@@ -232,3 +232,36 @@ def test_bf16_rescale_paths_vs_torch(cuda, kscale):
     ref = _torch_ref(q, k, v, dense, bs, S)
     err = rel_rows(out[:S].float().cpu().numpy(), ref[:S].cpu().numpy())
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("dynamic", [False, True])
+def test_sparse_layer_host_equals_device_path(cuda, dynamic):
+    """rp_sparse_layer_host (host Q/K/V -> H2D by head chunks -> mask from the
+    plan (dynamic: scored from the first chunk's heads) -> row lists ->
+    attention per chunk -> D2H) equals the device entry points."""
+    g = rp.make_grid(6, 512, 128)
+    if dynamic:
+        cfg = rp.SparsityConfig(rp.Mode.DynamicThreshold, rp.RadialParams(1.4, 0.7), 0.7, 0.45,
+                                0.0, 0.05)
+    else:
+        cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(2.0, 0.3), 0.75, 0.2,
+                                0.3, 0.3)
+    H, d = 6, 128
+    fb = rp.random_batch(g.total_tokens, H, d, 42)
+    q, k, v = fb.queries, fb.keys, fb.values
+    plan = rp.Plan(g, cfg, 7)
+    nsc = 2 if dynamic else 0
+    mask = plan.build_mask_device(q, k, 2) if dynamic else plan.build_mask_device()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mask)
+    want = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order)
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    mh = torch.zeros((g.blocks_per_dim, g.row_bytes), dtype=torch.uint8)
+    rp.profile_stages(True)
+    got = rp.sparse_layer_host(plan, qh, kh, vh, nsc, mask_out=mh)
+    prof = rp.profile_read()
+    rp.profile_stages(False)
+    assert torch.equal(mh, mask.cpu())
+    assert torch.equal(got, want.cpu())
+    assert prof["attention"][1] >= 1 and prof["csr"][1] == 1
+    if dynamic:
+        assert prof["score_select"][1] == 1 and prof["score_stats"][1] == 1
