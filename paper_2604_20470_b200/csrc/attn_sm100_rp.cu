@@ -10,10 +10,14 @@
 // and the tensor core's operand reads compete with the TMA writes for shared
 // memory (ablation: skipping the K/V reloads makes the db kernel 16 % faster).
 // Neighbouring block rows of a radial mask attend almost the same KV blocks,
-// so a CTA here owns the row PAIR (2p, 2p+1) of one head and walks the union
-// of their block lists: a K/V tile is loaded once and used by both query
-// tiles (S_A / S_B and P_A V / P_B V are issued only for the tiles whose list
-// holds the block -- no masked work).
+// so a CTA here owns the row PAIR (2p, 2p+1) of one head and walks their
+// blocks as ENTRIES (pair_fill_kernel): first the blocks both rows hold (one
+// K/V load used by both query tiles), then "split" entries pairing A's i-th
+// exclusive block with B's (two loads, one per tile), then the leftovers.
+// S_A / S_B and P_A V / P_B V are issued only for the tiles an entry holds --
+// no masked work -- and every two-tile entry keeps the tiles in ping-pong
+// (round 2: split entries instead of the sorted union, Hunyuan stage (d)
+// 1076 -> 1135 TFLOP/s).
 //
 // TMEM (512 columns): S_A 0-127, S_B 128-255, O_A 256-(256+D), O_B 384-(384+D);
 // P_x (bf16) overwrites the first 64 columns of S_x and is the A operand of
@@ -53,8 +57,9 @@ struct Layout {
 struct Params {
   const int32_t* row_ptr;   // per block row (own list lengths)
   const int32_t* prow_ptr;  // per row pair: union list offsets
-  const int32_t* pcol;      // union columns, ascending
-  const uint8_t* pflag;     // bit 0: row 2p holds it, bit 1: row 2p+1 holds it
+  const int32_t* pcol;      // per entry: (block of row 2p, block of row 2p+1), see pair_fill
+  const uint8_t* pflag;     // bit 0: row 2p active, bit 1: row 2p+1 active, bit 2: split
+                            // entry (the two rows take DIFFERENT blocks, two K/V loads)
   const int32_t* porder;    // pairs by descending union size (may be null)
   int n_rows;               // S_b
   int n_pairs;              // ceil(S_b / 2)
@@ -114,16 +119,27 @@ __global__ void pair_count_kernel(const int32_t* __restrict__ row_ptr,
   const int a = 2 * p, b = 2 * p + 1;
   int i = row_ptr[a], ie = row_ptr[a + 1];
   int j = b < n_rows ? row_ptr[b] : 0, je = b < n_rows ? row_ptr[b + 1] : 0;
-  int n = 0;
+  int nc = 0, na = 0, nb = 0;
   while (i < ie || j < je) {
     const int ca = i < ie ? col[i] : 0x7FFFFFFF, cb = j < je ? col[j] : 0x7FFFFFFF;
+    if (ca == cb) ++nc;
+    else if (ca < cb) ++na;
+    else ++nb;
     i += ca <= cb;
     j += cb <= ca;
-    ++n;
   }
-  counts[p] = n;
+  counts[p] = nc + (na > nb ? na : nb);  // entries: common, split pairs, leftovers
 }
 
+// Entry order of a row pair (A = 2p, B = 2p+1): first the blocks both rows
+// hold (ascending; one K/V load feeds both tiles), then the exclusive blocks
+// as SPLIT entries (A's i-th exclusive block with B's i-th: two K/V loads,
+// one per tile), then the leftover exclusive blocks of the longer list.
+// Online softmax is order-independent up to rounding; the order decides the
+// schedule.  In every entry with both tiles active the MMA warp issues
+// P_A.V, S_A, P_B.V, S_B, so the two tiles' softmax and MMAs ping-pong; in
+// the sorted union order used before, runs of one-tile entries exposed a
+// tile's softmax -> P.V -> S chain (Wan: 16.5 % of the tile steps).
 __global__ void pair_fill_kernel(const int32_t* __restrict__ row_ptr,
                                  const int32_t* __restrict__ col, int n_rows, int n_pairs,
                                  const int32_t* __restrict__ prow_ptr, int32_t* __restrict__ pcol,
@@ -131,17 +147,45 @@ __global__ void pair_fill_kernel(const int32_t* __restrict__ row_ptr,
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const int a = 2 * p, b = 2 * p + 1;
-  int i = row_ptr[a], ie = row_ptr[a + 1];
-  int j = b < n_rows ? row_ptr[b] : 0, je = b < n_rows ? row_ptr[b + 1] : 0;
-  int o = prow_ptr[p];
-  while (i < ie || j < je) {
-    const int ca = i < ie ? col[i] : 0x7FFFFFFF, cb = j < je ? col[j] : 0x7FFFFFFF;
-    const bool ta = ca <= cb, tb = cb <= ca;
-    pcol[o] = ta ? ca : cb;
-    pflag[o] = static_cast<uint8_t>((ta ? 1 : 0) | (tb ? 2 : 0));
-    i += ta;
-    j += tb;
-    ++o;
+  const int ia = row_ptr[a], iae = row_ptr[a + 1];
+  const int ib = b < n_rows ? row_ptr[b] : 0, ibe = b < n_rows ? row_ptr[b + 1] : 0;
+  int nc = 0, na = 0, nb = 0;
+  for (int i = ia, j = ib; i < iae || j < ibe;) {
+    const int ca = i < iae ? col[i] : 0x7FFFFFFF, cb = j < ibe ? col[j] : 0x7FFFFFFF;
+    if (ca == cb) ++nc;
+    else if (ca < cb) ++na;
+    else ++nb;
+    i += ca <= cb;
+    j += cb <= ca;
+  }
+  const int o = prow_ptr[p];
+  const int m = na < nb ? na : nb;
+  for (int e = nc; e < nc + (na > nb ? na : nb); ++e) {  // split / leftover entries
+    pcol[2 * (o + e)] = -1;
+    pcol[2 * (o + e) + 1] = -1;
+    pflag[o + e] = 0;
+  }
+  int kc = 0, ka = 0, kb = 0;
+  for (int i = ia, j = ib; i < iae || j < ibe;) {
+    const int ca = i < iae ? col[i] : 0x7FFFFFFF, cb = j < ibe ? col[j] : 0x7FFFFFFF;
+    if (ca == cb) {
+      pcol[2 * (o + kc)] = ca;
+      pcol[2 * (o + kc) + 1] = ca;
+      pflag[o + kc] = 3;
+      ++kc;
+    } else if (ca < cb) {
+      const int e = o + nc + (ka < m ? ka : m + (ka - m));
+      pcol[2 * e] = ca;
+      pflag[e] |= ka < m ? 1 | 4 : 1;
+      ++ka;
+    } else {
+      const int e = o + nc + (kb < m ? kb : m + (kb - m));
+      pcol[2 * e + 1] = cb;
+      pflag[e] |= kb < m ? 2 | 4 : 2;
+      ++kb;
+    }
+    i += ca <= cb;
+    j += cb <= ca;
   }
 }
 
@@ -230,14 +274,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                           w.h, w.row[x] * kBM, pol_q);
           ++ucnt[x];
         }
-        const int32_t* cols = p.pcol + w.beg;
-        int prev = 0;
+        // ring order per entry e: V of entry e-1 (A's, then B's if split),
+        // then K of entry e (likewise) -- the MMA warp's consumption order
+        const int32_t* cols = p.pcol + 2 * w.beg;
+        const uint8_t* flags = p.pflag + w.beg;
+        int pa = 0, pb = 0;
+        uint32_t pfl = 0;
         for (int e = 0; e <= w.n; ++e) {
-          if (e > 0) load_kv(&tv, w.h, prev);
+          if (e > 0) {
+            if (pfl & 4) {
+              load_kv(&tv, w.h, pa);
+              load_kv(&tv, w.h, pb);
+            } else {
+              load_kv(&tv, w.h, (pfl & 1) ? pa : pb);
+            }
+          }
           if (e < w.n) {
-            const int c = shfl0(__ldg(cols + e));
-            load_kv(&tk, w.h, c);
-            prev = c;
+            const uint32_t fl = static_cast<uint32_t>(shfl0(__ldg(flags + e)));
+            const int ca = shfl0(__ldg(cols + 2 * e));
+            const int cb = shfl0(__ldg(cols + 2 * e + 1));
+            if (fl & 4) {
+              load_kv(&tk, w.h, ca);
+              load_kv(&tk, w.h, cb);
+            } else {
+              load_kv(&tk, w.h, (fl & 1) ? ca : cb);
+            }
+            pa = ca;
+            pb = cb;
+            pfl = fl;
           }
         }
       }
@@ -258,21 +322,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t prev_fl = 0;
         for (int e = 0; e <= w.n; ++e) {
           const uint32_t fl = e < w.n ? static_cast<uint32_t>(shfl0(__ldg(flags + e))) : 0u;
-          // stages: V(e-1) then K(e), in ring order
-          uint32_t v_st = 0, k_st = 0;
-          if (e > 0) {
-            v_st = kv_it % L::kStages;
-            mbar_wait(&kv_full[v_st], (kv_it / L::kStages) & 1);
+          // ring slots: V of entry e-1 (two if it was split), then K of entry e
+          uint32_t v_st[2] = {0, 0}, k_st[2] = {0, 0};
+          auto take = [&]() {
+            const uint32_t st = kv_it % L::kStages;
+            mbar_wait(&kv_full[st], (kv_it / L::kStages) & 1);
             ++kv_it;
+            return st;
+          };
+          if (e > 0) {
+            v_st[0] = take();
+            v_st[1] = (prev_fl & 4) ? take() : v_st[0];
           }
           if (e < w.n) {
-            k_st = kv_it % L::kStages;
-            mbar_wait(&kv_full[k_st], (kv_it / L::kStages) & 1);
-            ++kv_it;
+            k_st[0] = take();
+            k_st[1] = (fl & 4) ? take() : k_st[0];
           }
           tc_fence_after();
-          const int last_pv = (prev_fl & 2) ? 1 : 0;  // tile issuing the last P.V on V(e-1)
-          const int last_s = (fl & 2) ? 1 : 0;
+          // a shared slot is released by its last user (B if B uses it); a
+          // split entry's slots have one user each
+          const int last_pv = ((prev_fl & 2) && !(prev_fl & 4)) ? 1 : 0;
+          const int last_s = ((fl & 2) && !(fl & 4)) ? 1 : 0;
 #pragma unroll
           for (int x = 0; x < 2; ++x) {
             if (e > 0 && (prev_fl >> x) & 1) {
@@ -281,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ++pcnt[x];
               if (done_pv[x] == 0) mbar_wait(&o_free[x], (ucnt[x] & 1) ^ 1);
               tc_fence_after();
-              const uint32_t vb = skv_addr + v_st * L::kTileBytes;
+              const uint32_t vb = skv_addr + v_st[x] * L::kTileBytes;
 #pragma unroll
               for (int kk = 0; kk < kBN / 16; ++kk)
                 umma_ts_w(tmem + L::o_col(x), tmem + L::s_col(x) + kk * 8,
@@ -289,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           done_pv[x] > 0 || kk > 0);
               ++done_pv[x];
               if (done_pv[x] == w.cnt[x]) umma_commit_w(&o_done[x]);
-              if (x == last_pv) umma_commit_w(&kv_empty[v_st]);
+              if ((prev_fl & 4) || x == last_pv) umma_commit_w(&kv_empty[v_st[x]]);
             }
             if (e < w.n && (fl >> x) & 1) {
               // S_x(e) = Q_x K(e)^T (overwrites P_x of its previous block,
@@ -297,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (done_s[x] == 0) mbar_wait(&q_full[x], ucnt[x] & 1);
               tc_fence_after();
               const uint32_t qa = sq_addr + x * L::kTileBytes;
-              const uint32_t kb = skv_addr + k_st * L::kTileBytes;
+              const uint32_t kb = skv_addr + k_st[x] * L::kTileBytes;
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t off = (kk / 4) * L::kChunkBytes + (kk % 4) * 32;
@@ -307,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ++done_s[x];
               umma_commit_w(&s_full[x]);
               if (done_s[x] == w.cnt[x]) umma_commit_w(&q_empty[x]);
-              if (x == last_s) umma_commit_w(&kv_empty[k_st]);
+              if ((fl & 4) || x == last_s) umma_commit_w(&kv_empty[k_st[x]]);
             }
           }
           prev_fl = fl;

@@ -105,9 +105,10 @@ static bool use_lpt_order() {
 // tile double-buffered in TMEM, Q in TMEM, two softmax warps per row.  "rp"
 // (attn_sm100_rp.cu): block-row pairs of one head sharing every K/V tile
 // over their union list.  DYNRAD_K6=db|rp forces one; the default (auto) is
-// db while one head's K + V fit in half of L2 and rp above that (measured:
-// Wan 75.8 k tokens, 38.8 MB per head: db 22.4 ms vs rp 24.2 ms; Hunyuan
-// 219.6 k tokens, 112 MB: db 109.2 ms vs rp 105.1 ms).
+// db while one head's K + V fit in half of L2 and rp above that (measured in
+// round 2, bench inputs: Wan 75.8 k tokens, 38.8 MB per head: db 22.0 ms vs
+// rp 23.4-23.8 ms; Hunyuan 219.6 k tokens, 112 MB: db 107 ms vs rp 101 ms;
+// DESIGN.md section 8).
 // Measured alternatives (incl. round 2's two-tile ping-pong "pp") live in
 // tools/experiments/k6_variants/.
 enum class K6Variant { kAuto, kDB, kRP };
@@ -200,7 +201,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       uint8_t* pflag = nullptr;
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcnt), sizeof(int32_t) * (n_pairs + 1), stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prow), sizeof(int32_t) * (n_pairs + 1), stream));
-      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcol), sizeof(int32_t) * cap, stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcol), sizeof(int32_t) * 2 * cap, stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pflag), cap, stream));
       const unsigned pg = static_cast<unsigned>((n_pairs + 127) / 128);
       attn3::pair_count_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, pcnt);
