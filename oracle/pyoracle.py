@@ -145,6 +145,7 @@ class _RefLib(_Lib):
         L.ref_masked_attention.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, _f32p, _f32p, _f32p,
                                            C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                            _f32p]
+        L.ref_expand_mask.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, _u8p]
         L.ref_random_batch.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, _f32p, _f32p,
                                        _f32p]
         L.ref_frame_pair.argtypes = [C.c_int, C.c_int, C.c_int, _P(_Cfg), C.c_int, C.c_int,
@@ -207,6 +208,14 @@ class _RefLib(_Lib):
         self._chk(self.lib.ref_masked_attention(nf, nt, bs, bits.ctypes.data_as(_u8p), _fp(q),
                                                 _fp(k), _fp(v), tok, h, d, int(exact), eps,
                                                 _fp(out)))
+        return out
+
+    def expand_mask(self, nf, nt, bs, bits):
+        _, padded, _, _ = grid_dims(nf, nt, bs)
+        out = np.zeros((padded, (padded + 7) // 8), np.uint8)
+        bits = np.ascontiguousarray(bits, np.uint8)
+        self._chk(self.lib.ref_expand_mask(nf, nt, bs, bits.ctypes.data_as(_u8p),
+                                           out.ctypes.data_as(_u8p)))
         return out
 
     def random_batch(self, tokens, heads, d, seed, with_values=True):
@@ -323,6 +332,8 @@ class _PortLib(_Lib):
                                       _P(C.c_double), C.c_int]
         L.orc_objective.argtypes = [_P(_Grid), _P(_Cfg), _f32p, C.c_int, C.c_uint64, C.c_double,
                                     C.c_double, _P(C.c_double), C.c_int]
+        L.orc_expand_mask.argtypes = [_P(_Grid), _u8p, _u8p]
+        L.orc_expand_mask.restype = None
         L.orc_random_batch.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, _f32p, _f32p,
                                        _f32p, C.c_int]
         L.orc_mix64.argtypes = [C.c_uint64]
@@ -406,6 +417,13 @@ class _PortLib(_Lib):
         self._chk(self.lib.orc_objective(C.byref(g), C.byref(c), _fp(f), f.shape[1], batch_seed,
                                          penalty_weight, sparsity_target, out, threads))
         return tuple(out)
+
+    def expand_mask(self, nf, nt, bs, bits):
+        g = self._grid(nf, nt, bs)
+        out = np.zeros((g.padded_tokens, (g.padded_tokens + 7) // 8), np.uint8)
+        bits = np.ascontiguousarray(bits, np.uint8)
+        self.lib.orc_expand_mask(C.byref(g), bits.ctypes.data_as(_u8p), out.ctypes.data_as(_u8p))
+        return out
 
     def random_batch(self, tokens, heads, d, seed, with_values=True, threads=1):
         q = np.zeros((tokens, heads, d), np.float32)

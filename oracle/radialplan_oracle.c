@@ -573,6 +573,22 @@ int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
                    threads);
 }
 
+/* expand_mask (mask.cpp:52-66): every active block's bit broadcast to its
+ * B x B token bits on the padded axis; out: padded_tokens rows of
+ * ceil(padded_tokens / 8) bytes, LSB-first (TokenMask, mask.hpp:39-55). */
+void orc_expand_mask(const orc_grid* g, const uint8_t* bits, uint8_t* out) {
+  const int64_t n = g->padded_tokens, trb = (n + 7) / 8;
+  memset(out, 0, (size_t)(n * trb));
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t br = r / g->block_size;
+    for (int64_t bc = 0; bc < g->blocks_per_dim; ++bc) {
+      if (!((bits[br * g->row_bytes + bc / 8] >> (bc % 8)) & 1u)) continue;
+      for (int64_t c = bc * g->block_size; c < (bc + 1) * g->block_size && c < n; ++c)
+        out[r * trb + c / 8] |= (uint8_t)(1u << (c % 8));
+    }
+  }
+}
+
 /* masked_attention (attention.cpp:107-113): epsilon must be positive. */
 int orc_masked_attention(const orc_grid* g, const uint8_t* bits, const float* q,
                          const float* k, const float* v, int64_t tokens, int heads, int d,

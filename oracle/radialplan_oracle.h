@@ -52,6 +52,7 @@ int orc_build_mask(const orc_grid* g, const orc_cfg* c, uint64_t seed,
  * [row_begin, row_end) of the padded axis.  q/k/v: [tokens, heads, d];
  * out: [(row_end-row_begin), heads, d].  Returns 3 on an empty row
  * (domain_error in the reference). */
+void orc_expand_mask(const orc_grid* g, const uint8_t* bits, uint8_t* out);
 int orc_masked_attention_exact(const orc_grid* g, const uint8_t* bits,
                                const float* q, const float* k, const float* v,
                                int64_t tokens, int heads, int d,

@@ -194,6 +194,17 @@ int ref_masked_attention(int nf, int nt, int bs, const std::uint8_t* bits,
   });
 }
 
+// expand_mask (mask.hpp:57, mask.cpp:52-66): the TokenMask bytes.
+int ref_expand_mask(int nf, int nt, int bs, const std::uint8_t* bits, std::uint8_t* out) {
+  return guarded([&] {
+    GridSpec g = make_grid(nf, nt, bs);
+    BlockMask bm(g.blocks_per_dim);
+    std::memcpy(bm.bits.data(), bits, bm.bits.size());
+    TokenMask tm = expand_mask(bm, g);
+    std::memcpy(out, tm.bits.data(), tm.bits.size());
+  });
+}
+
 // random_batch (attention.hpp:62): [tokens, heads, d] each; v may be NULL.
 int ref_random_batch(std::int64_t tokens, int heads, int d, std::uint64_t seed,
                      float* q, float* k, float* v) {

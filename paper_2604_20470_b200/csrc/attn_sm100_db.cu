@@ -93,6 +93,12 @@ struct Params {
   const uint8_t* soft_bits;
   long long soft_row_bytes;
   float soft_delta;
+  // B = 64 masks (QM kernels): the CSR is over 128 x 128 TILES (pairs of
+  // 64-blocks), qmask[entry] holds the tile's four 64 x 64 quadrant bits
+  // (bit 2 * row_half + key_half); out_rows = S' of the 64-block axis, rows
+  // at or beyond it exist only in the 128-row tile and are not written.
+  const uint8_t* qmask;
+  long long out_rows;
 };
 
 #ifdef RP_TRACE
@@ -193,7 +199,7 @@ __global__ void kmax_kernel(const __nv_bfloat16* __restrict__ k, long long token
   atomicMax(reinterpret_cast<int*>(kmax + h), __float_as_int(sqrtf(acc)));
 }
 
-template <int D>
+template <int D, bool QM = false>
 __global__ void __launch_bounds__(kThreads, 1)
     bsfa_fwd_db_kernel(const __grid_constant__ CUtensorMap tq,
                        const __grid_constant__ CUtensorMap tk,
@@ -433,10 +439,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = __ldg(p.row_ptr + row + 1) - beg;
       __nv_bfloat16* orow = p.out + (static_cast<long long>(row) * kBM + r) * p.out_tok_stride +
                             h * p.out_head_stride + half * (D / 2);
+      const bool row_out = !QM || static_cast<long long>(row) * kBM + r < p.out_rows;
       if (n == 0) {  // no active block: defined output (zeros); no pipeline traffic
         uint4 z = make_uint4(0, 0, 0, 0);
+        if (row_out) {
 #pragma unroll
-        for (int v = 0; v < D / 16; ++v) reinterpret_cast<uint4*>(orow)[v] = z;
+          for (int v = 0; v < D / 16; ++v) reinterpret_cast<uint4*>(orow)[v] = z;
+        }
         continue;
       }
       float m = -INFINITY;  // running max (raw logits), possibly stale
@@ -455,6 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int c = __ldg(p.col_idx + beg + j);
           const uint8_t by = __ldg(p.soft_bits + row * p.soft_row_bytes + (c >> 3));
           dlt = ((by >> (c & 7)) & 1) ? 0.f : p.soft_delta;
+        }
+        if constexpr (QM) {  // this thread's 64 keys are one 64 x 64 quadrant
+          const uint8_t qb = __ldg(p.qmask + beg + j);
+          if (!((qb >> ((r >= 64 ? 2 : 0) + half)) & 1)) dlt = -INFINITY;
         }
         if (tr) RP_TR2(0, g);
         mbar_wait(&s_full[b], (g >> 1) & 1);
@@ -483,11 +496,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
           return slot[r] + slot[128 + r];
         };
-        if (j == 0) {  // first block of the unit: the reference max comes first
+        // QM: a row may see no active key in its unit's first tiles (its
+        // quadrants masked); the reference max is taken from the first tile
+        // that has one (until then O and l stay zero).
+        if (j == 0 || (QM && __any_sync(0xFFFFFFFFu, m == -INFINITY))) {
           float a = S(0);
 #pragma unroll
           for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(S(i), S(i + 1)));
-          m = exchange_max(fmaxf(a, S(63)) + dlt);
+          const float mx = exchange_max(fmaxf(a, S(63)) + dlt);
+          m = (m == -INFINITY) ? mx : m;
           if (p.kmax_head) {
             // s = q.k <= |q||k| <= |q| max_t |k_t|: if that bound is within
             // 2^64 of the first block's max (the reference m only grows),
@@ -512,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float lmax = -INFINITY;
         auto exps = [&](float mref, bool track) {
           const float2 sc2 = make_float2(sl2, sl2);
-          const float nb = (dlt - mref) * sl2;
+          const float nb = (QM && mref == -INFINITY) ? -INFINITY : (dlt - mref) * sl2;
           const float2 ng2 = make_float2(nb, nb);
           acc[0] = acc[1] = make_float2(0.f, 0.f);
           float2 pv_prev[16];
@@ -638,13 +655,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(o_done, ord & 1);
       tc_fence_after();
       asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
-      const float inv = 1.0f / (red_l[r] + red_l[128 + r]);
+      const float lsum = red_l[r] + red_l[128 + r];
+      // QM: a row with no active key anywhere (the reference's domain_error,
+      // flagged from the 64-block CSR) is written as zeros
+      const float inv = QM ? (lsum > 0.f ? 1.0f / lsum : 0.f) : 1.0f / lsum;
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         uint32_t o[32];
         tmem_ld32(trow + L::kO + half * (D / 2) + c * 32, o);
         tmem_wait_ld();
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+        if (!row_out) continue;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           uint4 pkt;

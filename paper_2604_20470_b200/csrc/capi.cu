@@ -127,7 +127,10 @@ static K6Variant k6_variant(int64_t padded_tokens, int head_dim) {
   const double kv_head_bytes = 4.0 * static_cast<double>(padded_tokens) * head_dim;
   return kv_head_bytes > 64.0 * (1 << 20) ? K6Variant::kRP : K6Variant::kDB;
 }
-static const char* k6_kernel_name(int64_t padded_tokens, int head_dim) {
+static const char* k6_kernel_name(int64_t padded_tokens, int head_dim, int block_size) {
+  if (block_size == 64)
+    return head_dim == 64 ? "bsfa_fwd_db_kernel<64, quadrant mask>"
+                          : "bsfa_fwd_db_kernel<128, quadrant mask>";
   if (k6_variant(padded_tokens, head_dim) == K6Variant::kRP)
     return head_dim == 64 ? "bsfa_fwd_rp_kernel<64>" : "bsfa_fwd_rp_kernel<128>";
   return head_dim == 64 ? "bsfa_fwd_db_kernel<64>" : "bsfa_fwd_db_kernel<128>";
@@ -167,8 +170,8 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
   const float user_scale = scale;
   if (scale <= 0.f) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
   if (q.dtype == RP_BF16) {
-    if (g.block_size != 128)
-      throw std::invalid_argument("sparse attention (bf16): block_size must be 128");
+    if (g.block_size != 128 && g.block_size != 64)
+      throw std::invalid_argument("sparse attention (bf16): block_size must be 64 or 128");
     if (d != 64 && d != 128)
       throw std::invalid_argument("sparse attention (bf16): head_dim must be 64 or 128");
     for (const rp_tensor* t : {&q, &k, &v, static_cast<const rp_tensor*>(&o)})
@@ -192,6 +195,64 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
     const float soft_delta = soft_bits ? static_cast<float>((std::log(eps) - std::log1p(eps)) /
                                                             static_cast<double>(scale))
                                        : 0.f;
+    if (g.block_size == 64) {
+      // B = 64: the 128-row tensor-core tiles walk the merged
+      // lists of two 64-block rows; every tile carries its four 64 x 64
+      // quadrant bits and the db kernel masks the quadrants a thread's 64
+      // keys fall in (each softmax thread owns one 64-key half of a row).
+      if (soft_bits)
+        throw std::invalid_argument("soft-mask attention (bf16): block_size must be 128");
+      const int64_t nb = g.blocks_per_dim, ns = (nb + 1) / 2;
+      int32_t *scnt = nullptr, *srow = nullptr, *scol = nullptr;
+      uint8_t* qm = nullptr;
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scnt), sizeof(int32_t) * (ns + 1), stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&srow), sizeof(int32_t) * (ns + 1), stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scol), sizeof(int32_t) * ns * ns, stream));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&qm), ns * ns, stream));
+      const unsigned qg = static_cast<unsigned>((ns + 127) / 128);
+      csr::quad_kernel<false><<<qg, 128, 0, stream>>>(row_ptr, col_idx, nb, ns, scnt, nullptr,
+                                                       nullptr, nullptr);
+      RP_LAUNCHED();
+      csr::scan_kernel<<<1, 1024, 0, stream>>>(scnt, ns, srow, nullptr);
+      RP_LAUNCHED();
+      csr::quad_kernel<true><<<qg, 128, 0, stream>>>(row_ptr, col_idx, nb, ns, nullptr, srow,
+                                                      scol, qm);
+      RP_LAUNCHED();
+      attn2::Params p{};
+      p.row_ptr = srow;
+      p.col_idx = scol;
+      p.row_order = nullptr;
+      p.n_rows = static_cast<int>(ns);
+      p.heads = q.heads;
+      p.n_units = static_cast<long long>(q.heads) * ns;
+      p.out = static_cast<__nv_bfloat16*>(o.data);
+      p.out_tok_stride = o.token_stride;
+      p.out_head_stride = o.head_stride;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      p.qmask = qm;
+      p.out_rows = g.padded_tokens;
+      const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
+      if (d == 128) {
+        launch(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<128, true>),
+               attn2::Layout<128>::kSmemBytes, grid, attn2::kThreads, [&](int gr, int th, int sm) {
+                 attn2::bsfa_fwd_db_kernel<128, true><<<gr, th, sm, stream>>>(mq, mk, mv, p);
+               });
+      } else {
+        launch(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<64, true>),
+               attn2::Layout<64>::kSmemBytes, grid, attn2::kThreads, [&](int gr, int th, int sm) {
+                 attn2::bsfa_fwd_db_kernel<64, true><<<gr, th, sm, stream>>>(mq, mk, mv, p);
+               });
+      }
+      if (err_flag) {
+        csr::empty_row_flag_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, stream>>>(
+            row_ptr, nb, err_flag);
+        RP_LAUNCHED();
+      }
+      for (void* ptr : {static_cast<void*>(scnt), static_cast<void*>(srow),
+                        static_cast<void*>(scol), static_cast<void*>(qm)})
+        RP_CUDA(cudaFreeAsync(ptr, stream));
+      return;
+    }
     if (variant == K6Variant::kRP) {
       // union block lists of the row pairs (2p, 2p+1)
       const int n_rows = static_cast<int>(g.blocks_per_dim);
@@ -577,7 +638,7 @@ rp_status rp_random_batch(int64_t tokens, int heads, int head_dim, uint64_t seed
 
 const char* rp_attention_kernel(const rp_grid* g, int dtype, int head_dim) {
   if (dtype != RP_BF16) return "attn_f32_kernel";
-  return k6_kernel_name(g ? g->padded_tokens : 0, head_dim);
+  return k6_kernel_name(g ? g->padded_tokens : 0, head_dim, g ? g->block_size : 128);
 }
 
 rp_status rp_mask_to_csr(const rp_grid* g, const uint8_t* bits, int32_t* row_ptr,

@@ -146,6 +146,38 @@ __global__ void dense_lists_kernel(int64_t n, int32_t* __restrict__ row_ptr,
   if (i < n * n) col_idx[i] = static_cast<int32_t>(i % n);
 }
 
+// B = 64 masks on the 128-row tensor-core kernel: the 64-block CSR rows
+// (2R, 2R+1) merged into 128 x 128 tile row R (tile column C covers 64-block
+// columns 2C, 2C+1) with the tile's quadrant bits (bit 2 * row_half +
+// key_half).  One thread per tile row; the lists are sorted, c / 2 too.
+template <bool FILL>
+__global__ void quad_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                            int64_t nb, int64_t ns, int32_t* __restrict__ counts,
+                            const int32_t* __restrict__ srow_ptr, int32_t* __restrict__ scol,
+                            uint8_t* __restrict__ qmask) {
+  const int64_t R = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (R >= ns) return;
+  const int64_t a = 2 * R, b = 2 * R + 1;
+  int i = static_cast<int>(row_ptr[a]), ie = static_cast<int>(row_ptr[a + 1]);
+  int j = b < nb ? static_cast<int>(row_ptr[b]) : 0, je = b < nb ? static_cast<int>(row_ptr[b + 1]) : 0;
+  int n = 0;
+  int o = FILL ? srow_ptr[R] : 0;
+  while (i < ie || j < je) {
+    const int ca = i < ie ? col[i] >> 1 : 0x7FFFFFFF, cb = j < je ? col[j] >> 1 : 0x7FFFFFFF;
+    const int C = ca < cb ? ca : cb;
+    uint32_t q = 0;
+    while (i < ie && (col[i] >> 1) == C) q |= 1u << (col[i++] & 1);
+    while (j < je && (col[j] >> 1) == C) q |= 4u << (col[j++] & 1);
+    if (FILL) {
+      scol[o] = C;
+      qmask[o] = static_cast<uint8_t>(q);
+      ++o;
+    }
+    ++n;
+  }
+  if (!FILL) counts[R] = n;
+}
+
 // Flags a row without any active block (the reference's domain_error,
 // attention.cpp:85-86) for kernels that zero-fill such rows silently.
 __global__ void empty_row_flag_kernel(const int32_t* __restrict__ row_ptr, int64_t n,

@@ -265,3 +265,71 @@ def test_sparse_layer_host_equals_device_path(cuda, dynamic):
     assert prof["attention"][1] >= 1 and prof["csr"][1] == 1
     if dynamic:
         assert prof["score_select"][1] == 1 and prof["score_stats"][1] == 1
+
+
+def test_expand_mask_matches_reference_golden(cuda):
+    """rp_expand_mask on the device is byte-identical to
+    the reference's expand_mask (mask.cpp:52-66) -- golden TokenMask bytes
+    written by oracle/_ref (tests/golden/make_golden_expand.py), padded and
+    unpadded grids, B = 4 .. 128, static / dynamic / random block masks."""
+    import os
+    gz = np.load(os.path.join(os.path.dirname(__file__), "golden", "expand_mask.npz"))
+    for i in range(int(gz["n"])):
+        nf, nt, bs = (int(x) for x in gz[f"grid_{i}"])
+        g = rp.make_grid(nf, nt, bs)
+        got = rp.expand_mask(torch.from_numpy(gz[f"bits_{i}"]).cuda(), g).cpu().numpy()
+        np.testing.assert_array_equal(got, gz[f"token_{i}"], err_msg=f"case {i}")
+
+
+@pytest.mark.parametrize("nf,nt,heads,d,density,seed", [
+    (4, 300, 3, 128, 0.3, 1),    # S' = 1216 = 19 blocks of 64: odd, last tile half outside S'
+    (5, 256, 2, 64, 0.2, 2),     # 20 blocks, d = 64
+    (3, 1000, 2, 128, 0.05, 3),  # very sparse: rows whose first tiles are masked
+    (2, 192, 2, 128, 1.0, 4),    # dense
+])
+def test_bf16_block64_vs_fp32(cuda, nf, nt, heads, d, density, seed):
+    """SURVEY R3 / a18 at B = 64 on the tensor cores: 128-row tiles over the
+    merged lists of two 64-block rows with 64 x 64 quadrant masking, against
+    an fp32 evaluation of the B = 64 mask on the same bf16 inputs (2e-2)."""
+    g = rp.make_grid(nf, nt, 64)
+    S = g.total_tokens
+    torch.manual_seed(seed)
+    q, k, v = (torch.randn(S, heads, d, device="cuda").to(torch.bfloat16) for _ in range(3))
+    dense = _random_mask(g.blocks_per_dim, density, seed)
+    mdev = torch.from_numpy(pyoracle.pack_dense(dense)).cuda()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mdev)
+    out = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, check_empty=True)
+    assert out.shape[0] == g.padded_tokens
+    ref = _torch_ref(q, k, v, dense, 64, S)
+    err = rel_rows(out.float().cpu().numpy(), ref.cpu().numpy())
+    assert err < 2e-2, err
+    assert "quadrant" in rp.attention_kernel(g, "bf16", d)
+
+
+def test_bf16_block64_radial_mask_vs_oracle(cuda, port):
+    """B = 64 with a reference radial mask (static, built on the device and
+    bit-identical to the reference) against the C restatement of
+    masked_attention_exact on sampled rows."""
+    nf, nt, bs, H, d = 6, 400, 64, 2, 128
+    g = rp.make_grid(nf, nt, bs)
+    cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(2.0, 0.3), 0.75, 0.2, 0.3, 0.3)
+    mask = rp.Plan(g, cfg, 7).build_mask_device()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mask)
+    fb = rp.random_batch(g.total_tokens, H, d, 42)
+    out = rp.sparse_attention(g, fb.queries, fb.keys, fb.values, row_ptr, col_idx, order)
+    qn, kn, vn = (t.float().cpu().numpy() for t in (fb.queries, fb.keys, fb.values))
+    ref = port.masked_attention_exact(nf, nt, bs, mask.cpu().numpy(), qn, kn, vn, threads=8)
+    assert rel_rows(out.float().cpu().numpy(), ref) < 2e-2
+
+
+def test_bf16_block64_empty_row_is_domain_error(cuda):
+    g = rp.make_grid(2, 256, 64)
+    dense = np.eye(g.blocks_per_dim, dtype=np.uint8)
+    dense[3, 3] = 0
+    row_ptr, col_idx, order = rp.mask_to_csr(g, torch.from_numpy(pyoracle.pack_dense(dense)).cuda())
+    q, k, v = (torch.randn(512, 2, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
+    with pytest.raises(rp.DomainError):
+        rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, check_empty=True)
+    out = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order)
+    assert torch.count_nonzero(out[192:256]) == 0
+    assert bool(torch.isfinite(out.float()).all())

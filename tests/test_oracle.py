@@ -164,3 +164,14 @@ def test_objective_restatement_vs_reference_random(ref, port):
                   float(rng.uniform(-1, 1)) if mode else float(rng.uniform(0.3, 1)), far, 1)
         want = ref.objective(nf, nt, bs, cfg, f, 7 + trial)
         assert port.objective(nf, nt, bs, cfg, f, 7 + trial, threads=2) == want
+
+
+def test_expand_mask_port_matches_reference_golden(port):
+    """The C restatement's expand_mask equals the reference's own TokenMask
+    bytes (tests/golden/expand_mask.npz, made by oracle/_ref)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "expand_mask.npz"))
+    for i in range(int(g["n"])):
+        nf, nt, bs = (int(x) for x in g[f"grid_{i}"])
+        np.testing.assert_array_equal(port.expand_mask(nf, nt, bs, g[f"bits_{i}"]),
+                                      g[f"token_{i}"])
