@@ -121,11 +121,20 @@ static K6Variant k6_forced() {
   }();
   return v;
 }
+// The auto rule's threshold in MiB of K + V per head (DYNRAD_K6_RP_MIN_MB,
+// default 64: half of L2); tests lower it to run the auto path on small grids.
+static double k6_rp_min_bytes() {
+  static const double b = [] {
+    const char* e = std::getenv("DYNRAD_K6_RP_MIN_MB");
+    return (e ? std::atof(e) : 64.0) * (1 << 20);
+  }();
+  return b;
+}
 static K6Variant k6_variant(int64_t padded_tokens, int head_dim) {
   const K6Variant f = k6_forced();
   if (f != K6Variant::kAuto) return f;
   const double kv_head_bytes = 4.0 * static_cast<double>(padded_tokens) * head_dim;
-  return kv_head_bytes > 64.0 * (1 << 20) ? K6Variant::kRP : K6Variant::kDB;
+  return kv_head_bytes > k6_rp_min_bytes() ? K6Variant::kRP : K6Variant::kDB;
 }
 static const char* k6_kernel_name(int64_t padded_tokens, int head_dim, int block_size) {
   if (block_size == 64)

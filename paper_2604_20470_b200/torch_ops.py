@@ -80,6 +80,7 @@ class RadialSparseAttention(torch.nn.Module):
         self.n_score_heads = n_score_heads
         self.softmax_scale = softmax_scale
         self._lists: Optional[tuple] = None
+        self._bufs: Optional[tuple] = None  # dynamic mode: mask + row-list buffers, per device
 
     @property
     def dynamic(self) -> bool:
@@ -87,8 +88,18 @@ class RadialSparseAttention(torch.nn.Module):
 
     def block_lists(self, q: Optional[torch.Tensor] = None, k: Optional[torch.Tensor] = None):
         if self.dynamic:
-            mask = self.plan.build_mask_device(q, k, self.n_score_heads)
-            return rp.mask_to_csr(self.grid, mask)
+            # no host sync per layer: module-owned buffers, untrimmed lists
+            # (row_ptr delimits them), so the layer can be graph-captured
+            g = self.grid
+            nb = g.blocks_per_dim
+            if self._bufs is None or self._bufs[0].device != q.device:
+                self._bufs = (torch.empty((nb, g.row_bytes), dtype=torch.uint8, device=q.device),
+                              (torch.empty(nb + 1, dtype=torch.int32, device=q.device),
+                               torch.empty(nb * nb, dtype=torch.int32, device=q.device),
+                               torch.empty(nb, dtype=torch.int32, device=q.device),
+                               torch.zeros(1, dtype=torch.int64, device=q.device)))
+            mask = self.plan.build_mask_device(q, k, self.n_score_heads, out=self._bufs[0])
+            return rp.mask_to_csr(self.grid, mask, out=self._bufs[1])
         if self._lists is None:
             self._lists = rp.mask_to_csr(self.grid, self.plan.build_mask_device())
         return self._lists

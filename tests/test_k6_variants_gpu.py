@@ -22,3 +22,22 @@ def test_variant_passes_attention_parity(cuda, variant):
                         "-k", "bf16 or wan_shape or empty_row or host_pipeline"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_auto_rule_above_threshold_runs_rp(cuda):
+    """The default (auto) kernel choice switches to rp above the K + V-per-
+    head threshold; with the threshold lowered (DYNRAD_K6_RP_MIN_MB=0) the
+    default environment takes that path on the test grids and stays within
+    tolerance, and the library reports the kernel it launches."""
+    env = dict(os.environ, DYNRAD_K6_RP_MIN_MB="0")
+    env.pop("DYNRAD_K6", None)
+    code = ("import sys; sys.path.insert(0, %r); from paper_2604_20470_b200 import radialplan as rp;"
+            "print(rp.attention_kernel(rp.make_grid(4, 300, 128)))" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "rp_kernel" in r.stdout, r.stdout + r.stderr
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_attention_gpu.py"),
+                        "-k", "bf16_kernel or wan_shape or host_pipeline or layer_host"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
