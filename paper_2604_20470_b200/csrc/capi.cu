@@ -507,10 +507,6 @@ int64_t rp_kernel_launch_count(void) { return g_launches.load(); }
 int rp_debug_trace(void* host) {
   return cudaMemcpyFromSymbol(host, attn2::g_trace, sizeof(attn2::g_trace)) == cudaSuccess ? 0 : 1;
 }
-int rp_debug_trace_pp(void* host) {
-  return cudaMemcpyFromSymbol(host, attn9::g_trace_pp, sizeof(attn9::g_trace_pp)) == cudaSuccess
-             ? 0 : 1;
-}
 #endif
 
 rp_status rp_make_grid(int nf, int nt, int bs, rp_grid* out) {

@@ -6,12 +6,10 @@ from paper_2604_20470_b200 import radialplan as rp, _lib
 from oracle import pyoracle
 g = rp.make_grid(21, 3600, 128)
 H, d = 40, 128
-q = torch.randn(g.total_tokens, H, d, device="cuda", dtype=torch.bfloat16)
-k = torch.randn_like(q); v = torch.randn_like(q)
-nb = g.blocks_per_dim
-dense = (np.random.default_rng(0).random((nb, nb)) < 0.194).astype(np.uint8)
-np.fill_diagonal(dense, 1)
-rowp, coli, order = rp.mask_to_csr(g, torch.from_numpy(pyoracle.pack_dense(dense)).cuda())
+fb = rp.random_batch(g.total_tokens, H, d, 42)   # the bench's inputs and mask
+q, k, v = fb.queries, fb.keys, fb.values
+cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(1.0, 0.1), 1.0, 0.2, 0.3, 0.3)
+rowp, coli, order = rp.mask_to_csr(g, rp.Plan(g, cfg, 7).build_mask_device())
 out = torch.empty((g.padded_tokens, H, d), device="cuda", dtype=torch.bfloat16)
 for _ in range(2):
     rp.sparse_attention(g, q, k, v, rowp, coli, order, out=out)
