@@ -94,8 +94,9 @@ def compare(g, q, k, v, row_ptr, col_idx, order, H, Hl, d, reps=3):
         x = torch.zeros((1, Sp, Hl, d), dtype=torch.bfloat16, device=q.device)
         x[0, :S] = t
         pads.append(x)
+    nnz = int(row_ptr[-1].item())  # col_idx may be an untrimmed buffer (dynamic layers)
+    col_idx = col_idx[:nnz]
     rows = _lists(row_ptr, col_idx, nb)
-    nnz = int(col_idx.numel())
     flops_of = lambda n: 4.0 * H * d * g.block_size ** 2 * n  # noqa: E731
     scale = H / Hl
     recs = {}
