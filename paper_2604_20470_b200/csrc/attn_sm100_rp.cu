@@ -78,6 +78,39 @@ struct Params {
   float soft_delta;
 };
 
+// Per-entry metadata (flags, block pair) read 32 entries at a time by the
+// whole warp (lane i: entry base + i) with the next 32 prefetched, and
+// broadcast per entry: a dependent global load per entry sat on the producer
+// and MMA issue paths (~0.5 us each).
+struct EntryStream {
+  const uint8_t* flags;
+  const int2* cols;
+  int n, base = -1;
+  uint32_t f_cur = 0, f_nxt = 0;
+  int2 c_cur = make_int2(0, 0), c_nxt = make_int2(0, 0);
+  RP_DEV void load(int b, uint32_t& f, int2& c) const {
+    const int e = b + (threadIdx.x & 31);
+    f = e < n ? __ldg(flags + e) : 0u;
+    c = e < n && cols ? __ldg(cols + e) : make_int2(0, 0);
+  }
+  RP_DEV void at(int e, uint32_t* fl, int* ca, int* cb) {
+    const int b = e & ~31;
+    if (b != base) {
+      if (base >= 0 && b == base + 32) {
+        f_cur = f_nxt;
+        c_cur = c_nxt;
+      } else {
+        load(b, f_cur, c_cur);
+      }
+      load(b + 32, f_nxt, c_nxt);
+      base = b;
+    }
+    *fl = __shfl_sync(0xFFFFFFFFu, f_cur, e & 31);
+    if (ca) *ca = __shfl_sync(0xFFFFFFFFu, c_cur.x, e & 31);
+    if (cb) *cb = __shfl_sync(0xFFFFFFFFu, c_cur.y, e & 31);
+  }
+};
+
 struct Unit {
   int h, p, row[2], beg, n, cnt[2];
   bool has[2];
@@ -276,8 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // ring order per entry e: V of entry e-1 (A's, then B's if split),
         // then K of entry e (likewise) -- the MMA warp's consumption order
-        const int32_t* cols = p.pcol + 2 * w.beg;
-        const uint8_t* flags = p.pflag + w.beg;
+        EntryStream es{p.pflag + w.beg, reinterpret_cast<const int2*>(p.pcol) + w.beg, w.n};
         int pa = 0, pb = 0;
         uint32_t pfl = 0;
         for (int e = 0; e <= w.n; ++e) {
@@ -290,9 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (e < w.n) {
-            const uint32_t fl = static_cast<uint32_t>(shfl0(__ldg(flags + e)));
-            const int ca = shfl0(__ldg(cols + 2 * e));
-            const int cb = shfl0(__ldg(cols + 2 * e + 1));
+            uint32_t fl;
+            int ca, cb;
+            es.at(e, &fl, &ca, &cb);
             if (fl & 4) {
               load_kv(&tk, w.h, ca);
               load_kv(&tk, w.h, cb);
@@ -317,11 +349,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (long long u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Unit w = decode(p, u, true);
         if (w.n == 0) continue;
-        const uint8_t* flags = p.pflag + w.beg;
+        EntryStream es{p.pflag + w.beg, nullptr, w.n};
         int done_s[2] = {0, 0}, done_pv[2] = {0, 0};
         uint32_t prev_fl = 0;
         for (int e = 0; e <= w.n; ++e) {
-          const uint32_t fl = e < w.n ? static_cast<uint32_t>(shfl0(__ldg(flags + e))) : 0u;
+          uint32_t fl = 0u;
+          if (e < w.n) es.at(e, &fl, nullptr, nullptr);
           // ring slots: V of entry e-1 (two if it was split), then K of entry e
           uint32_t v_st[2] = {0, 0}, k_st[2] = {0, 0};
           auto take = [&]() {
