@@ -3,11 +3,14 @@
 ms per layer, TFLOP/s on active blocks and fraction of the measured bf16 peak,
 next to dense bf16 attention (our kernel on a full mask, and torch SDPA).
 Static-ratio masks (SURVEY 6.3 points; 90-95 % is unreachable under the
-reference semantics).  Writes one JSON document to stdout."""
+reference semantics), at B = 128 and, for the config-3 knobs,
+B = 64 too; the bench's random_batch inputs; NVML clocks sampled over the
+whole sweep (bench.ClockSampler).  Writes one JSON document to stdout."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
+from bench import ClockSampler, FEATURE_SEED  # noqa: E402
 from paper_2604_20470_b200 import radialplan as rp
 
 POINTS = [  # gamma, lambda, theta_m, theta_c, rho1, rho2   (reference sparsity, SURVEY 6.3)
@@ -38,36 +41,46 @@ def timed(fn, reps=5):
 def main():
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["bf16_tflops"]
+    H, d = 40, 128
     g = rp.make_grid(21, 3600, 128)
-    H, d, S = 40, 128, g.total_tokens
-    gen = torch.Generator(device="cuda").manual_seed(42)
-    q, k, v = (torch.randn((S, H, d), device="cuda", generator=gen).to(torch.bfloat16)
-               for _ in range(3))
-    out = torch.empty((g.padded_tokens, H, d), device="cuda", dtype=torch.bfloat16)
-    nb = g.blocks_per_dim
-    full = torch.from_numpy(np.packbits(np.ones((nb, nb), np.uint8), axis=1,
-                                        bitorder="little")).cuda()
-    rpf, cif, orf = rp.mask_to_csr(g, full)
-    dense_ms = timed(lambda: rp.sparse_attention(g, q, k, v, rpf, cif, orf, out=out), 2)
-    qs, ks, vs = (t.permute(1, 0, 2).unsqueeze(0) for t in (q, k, v))
-    sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs), 2)
+    S = g.total_tokens
+    fb = rp.random_batch(S, H, d, FEATURE_SEED)
+    q, k, v = fb.queries, fb.keys, fb.values
     rows = []
-    for (gm, lm, tm, tc, a, b) in POINTS:
-        cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(gm, lm), tm, tc, a, b)
-        mask = rp.Plan(g, cfg, 7).build_mask_device()
-        row_ptr, col_idx, order = rp.mask_to_csr(g, mask)
-        nnz = int(col_idx.numel())
-        ms = timed(lambda: rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order, out=out))
-        tf = 4.0 * H * d * 128 * 128 * nnz / (ms * 1e-3) / 1e12
-        rows.append({"gamma": gm, "lambda": lm, "theta_m": tm, "theta_c": tc, "rho": [a, b],
-                     "block_sparsity": round(1 - nnz / nb / nb, 4), "nnz": nnz,
-                     "ms_per_layer": round(ms, 3), "tflops_active": round(tf, 1),
-                     "frac_of_peak": round(tf / peak, 4),
-                     "speedup_vs_ours_dense": round(dense_ms / ms, 2),
-                     "speedup_vs_sdpa": round(sdpa_ms / ms, 2)})
-    print(json.dumps({"workload": "Wan2.1-14B 21x45x80, 40 heads, d=128, bf16, B=128, 1 GPU",
+    with ClockSampler(0) as clk:
+        out = torch.empty((g.padded_tokens, H, d), device="cuda", dtype=torch.bfloat16)
+        nb = g.blocks_per_dim
+        full = torch.from_numpy(np.packbits(np.ones((nb, nb), np.uint8), axis=1,
+                                            bitorder="little")).cuda()
+        rpf, cif, orf = rp.mask_to_csr(g, full)
+        dense_ms = timed(lambda: rp.sparse_attention(g, q, k, v, rpf, cif, orf, out=out), 2)
+        qs, ks, vs = (t.permute(1, 0, 2).unsqueeze(0) for t in (q, k, v))
+        sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs), 2)
+        for bs, points in ((128, POINTS), (64, [POINTS[5]])):
+            gb = rp.make_grid(21, 3600, bs)
+            nbb = gb.blocks_per_dim
+            outb = torch.empty((gb.padded_tokens, H, d), device="cuda", dtype=torch.bfloat16)
+            for (gm, lm, tm, tc, a, b) in points:
+                cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(gm, lm), tm, tc, a, b)
+                mask = rp.Plan(gb, cfg, 7).build_mask_device()
+                row_ptr, col_idx, order = rp.mask_to_csr(gb, mask)
+                nnz = int(col_idx.numel())
+                ms = timed(lambda: rp.sparse_attention(gb, q, k, v, row_ptr, col_idx, order,
+                                                       out=outb))
+                tf = 4.0 * H * d * bs * bs * nnz / (ms * 1e-3) / 1e12
+                rows.append({"block_size": bs, "gamma": gm, "lambda": lm, "theta_m": tm,
+                             "theta_c": tc, "rho": [a, b],
+                             "block_sparsity": round(1 - nnz / nbb / nbb, 4), "nnz": nnz,
+                             "kernel": rp.attention_kernel(gb, "bf16", d),
+                             "ms_per_layer": round(ms, 3), "tflops_active": round(tf, 1),
+                             "frac_of_peak": round(tf / peak, 4),
+                             "speedup_vs_ours_dense": round(dense_ms / ms, 2),
+                             "speedup_vs_sdpa": round(sdpa_ms / ms, 2)})
+    print(json.dumps({"workload": "Wan2.1-14B 21x45x80, 40 heads, d=128, bf16, 1 GPU, "
+                                  "random_batch(S, 40, 128, 42) inputs",
                       "peak_bf16_tflops": peak, "dense_ours_ms": round(dense_ms, 2),
-                      "dense_sdpa_ms": round(sdpa_ms, 2), "points": rows}, indent=1))
+                      "dense_sdpa_ms": round(sdpa_ms, 2), "clocks": clk.summary(),
+                      "points": rows}, indent=1))
 
 
 if __name__ == "__main__":
