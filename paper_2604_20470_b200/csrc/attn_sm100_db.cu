@@ -179,24 +179,45 @@ struct Cursor {
 // max_t |k_t| per head (the logit bound of the exchange-free rescale
 // protocol): one thread per (token, head), 16-byte loads, fp32 sum of squares,
 // atomicMax on the non-negative float's bits.
+// max_t |k_t| per head (the logit bound of the exchange-free rescale
+// protocol): one warp per token in a grid-stride loop, lane l owns heads
+// l, l + 32 (heads <= 64) and keeps their running max in registers; the
+// block then reduces through shared memory and issues one atomicMax per
+// (block, head).  One read of K (HBM-bound).
 __global__ void kmax_kernel(const __nv_bfloat16* __restrict__ k, long long tokens, int heads,
                             int d, long long ts, long long hs, float* __restrict__ kmax) {
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= tokens * heads) return;
-  const long long t = i / heads;
-  const int h = static_cast<int>(i % heads);
-  const uint4* row = reinterpret_cast<const uint4*>(k + t * ts + h * hs);
-  float acc = 0.f;
-  for (int c = 0; c < d / 8; ++c) {
-    const uint4 u = __ldg(row + c);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  __shared__ int red[64];
+  for (int h = threadIdx.x; h < 64; h += blockDim.x) red[h] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  float m0 = 0.f, m1 = 0.f;
+  for (long long t = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       t < tokens; t += warps) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
-      acc = fmaf(lo, lo, fmaf(hi, hi, acc));
+    for (int x = 0; x < 2; ++x) {
+      const int h = lane + 32 * x;
+      if (h >= heads) continue;
+      const uint4* row = reinterpret_cast<const uint4*>(k + t * ts + h * hs);
+      float acc = 0.f;
+      for (int c = 0; c < d / 8; ++c) {
+        const uint4 u = __ldg(row + c);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
+          acc = fmaf(lo, lo, fmaf(hi, hi, acc));
+        }
+      }
+      if (x == 0) m0 = fmaxf(m0, acc);
+      else m1 = fmaxf(m1, acc);
     }
   }
-  atomicMax(reinterpret_cast<int*>(kmax + h), __float_as_int(sqrtf(acc)));
+  if (lane < heads) atomicMax(&red[lane], __float_as_int(sqrtf(m0)));
+  if (lane + 32 < heads) atomicMax(&red[lane + 32], __float_as_int(sqrtf(m1)));
+  __syncthreads();
+  for (int h = threadIdx.x; h < heads; h += blockDim.x)
+    atomicMax(reinterpret_cast<int*>(kmax + h), red[h]);
 }
 
 template <int D, bool QM = false>

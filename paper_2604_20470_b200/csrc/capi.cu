@@ -346,6 +346,25 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       p.soft_bits = soft_bits;
       p.soft_row_bytes = g.row_bytes;
       p.soft_delta = soft_delta;
+      // Exchange-free rescale protocol (DYNRAD_DB_LAG=1): a per-head max |k|
+      // pre-pass (one read of K) bounds every logit, so units whose bound
+      // stays within 2^64 of their first block's max decide rescales two
+      // steps late from the halves' block sums, without the per-step
+      // exchange barrier (attn_sm100_db.cu).
+      static const bool lag_on = [] {
+        const char* e = std::getenv("DYNRAD_DB_LAG");
+        return e && std::strcmp(e, "1") == 0;
+      }();
+      float* kmax = nullptr;
+      if (lag_on && !soft_bits && k.head_dim % 8 == 0 && k.heads <= 64) {
+        RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kmax), sizeof(float) * k.heads, stream));
+        RP_CUDA(cudaMemsetAsync(kmax, 0, sizeof(float) * k.heads, stream));
+        attn2::kmax_kernel<<<sm_count() * 2, 256, 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(k.data), k.tokens, k.heads, k.head_dim,
+            k.token_stride, k.head_stride, kmax);
+        RP_LAUNCHED();
+        p.kmax_head = kmax;
+      }
       const int grid = static_cast<int>(std::min<long long>(p.n_units, sm_count()));
       if (d == 128) {
         launch(reinterpret_cast<const void*>(attn2::bsfa_fwd_db_kernel<128>),
@@ -358,6 +377,7 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
                  attn2::bsfa_fwd_db_kernel<64><<<gr, th, sm, stream>>>(mq, mk, mv, p);
                });
       }
+      if (kmax) RP_CUDA(cudaFreeAsync(kmax, stream));
       if (err_flag) {
         // db zero-fills empty rows without flagging them: flag from the CSR
         csr::empty_row_flag_kernel<<<static_cast<unsigned>((g.blocks_per_dim + 255) / 256), 256,
