@@ -35,8 +35,12 @@ namespace attn3 {
 constexpr int kThreads = 384;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
+// Pairs (of every 8 per 16-key chunk) whose exp2 runs as a polynomial on the
+// FMA pipe: 1 of 8 measured +1.1 % at the Hunyuan shape (bench, two
+// interleaved runs: 101.5-102.3 vs 102.9-103.4 ms), neutral at Wan; 2 of 8
+// was slower.
 #ifndef RP_RP_POLY_MASK
-#define RP_RP_POLY_MASK 0x00u
+#define RP_RP_POLY_MASK 0x01u
 #endif
 constexpr uint32_t kPolyMask = RP_RP_POLY_MASK;
 
