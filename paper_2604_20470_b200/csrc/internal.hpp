@@ -65,6 +65,12 @@ rp_status guarded(F&& f) {
 // running `check` (may be null) on it.
 void prepare_kernel(const void* fn, int smem, void (*check)(const void*) = nullptr);
 
+// Keep the stream-ordered pool's memory between calls on the current device
+// (the default release threshold returns every byte at each synchronize, so
+// the multi-GB scratch of a static mask build or a host-buffer layer would be
+// re-mapped on every call).
+void keep_pool_memory();
+
 // Optional per-stage CUDA-event timing (rp_profile_stages): when enabled,
 // library entry points bracket their kernels with events on the launching
 // stream; bench.py reads the per-stage device time of the timed region.

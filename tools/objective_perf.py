@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import pyoracle  # noqa: E402
 from oracle.pyoracle import Cfg  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 from paper_2604_20470_b200 import radialplan as rp  # noqa: E402
 
 GRIDS = [("cli_default_16x64_b16", 16, 64, 16, 64),
@@ -45,10 +46,20 @@ def timed(fn, reps):
     return a.elapsed_time(b) / reps
 
 
+def _cpu_objective(lib, nf, nt, bs, fh, threads):
+    c = Cfg(*STATIC[:8], STATIC[8])
+    if lib.kind == "reference":
+        return lib.objective(nf, nt, bs, c, fh, 5)
+    return lib.objective(nf, nt, bs, c, fh, 5, threads=threads)
+
+
 def main():
-    port = pyoracle.port()
-    threads = os.cpu_count() or 1
-    out = {"what": "profiler objective (SURVEY 8f3), GPU vs C restatement", "cpu_threads": threads,
+    # CPU side: the reference's own profiler objective (oracle/_ref, single
+    # threaded, its own S x S cache) when built, else the C restatement
+    port = pyoracle.ref() if pyoracle.have_ref() else pyoracle.port()
+    kind = "reference (oracle/_ref)" if pyoracle.have_ref() else "C restatement"
+    threads = 1 if pyoracle.have_ref() else (os.cpu_count() or 1)
+    out = {"what": "profiler objective (SURVEY 8f3), GPU trial vs CPU objective", "cpu_threads": threads,
            "grids": []}
     for name, nf, nt, bs, dim in GRIDS:
         g = rp.make_grid(nf, nt, bs)
@@ -61,25 +72,27 @@ def main():
             if "c" in holder:
                 holder["c"].close()
             holder["c"] = rp.ProxyCache(g, f)
-        cache_ms = timed(build, 3)
-        cache = holder["c"]
-        st = timed(lambda: cache.objective(cfg_rp(STATIC), 5), 5)
-        dy = timed(lambda: cache.objective(cfg_rp(DYNAMIC), 5, features=f), 3)
+        with ClockSampler(0) as clk:
+            cache_ms = timed(build, 3)
+            cache = holder["c"]
+            st = timed(lambda: cache.objective(cfg_rp(STATIC), 5), 5)
+            dy = timed(lambda: cache.objective(cfg_rp(DYNAMIC), 5, features=f), 3)
         rec = {"grid": name, "tokens": n, "feature_dim": dim, "gpu_cache_build_ms": cache_ms,
                "gpu_trial_static_ms": st, "gpu_trial_dynamic_ms": dy,
                "cache_bytes": n * ((n + bs - 1) // bs) * 16 + n * 20,
-               "reference_cache_bytes": n * n * 4 + n * 8}
+               "reference_cache_bytes": n * n * 4 + n * 8, "clocks": clk.summary(),
+               "cpu_kind": kind}
         fh = f.cpu().numpy()
         if n <= 4096:
             t0 = time.time()
-            port.objective(nf, nt, bs, Cfg(*STATIC[:8], STATIC[8]), fh, 5, threads=threads)
+            _cpu_objective(port, nf, nt, bs, fh, threads)
             rec["cpu_objective_s"] = time.time() - t0
             rec["cpu_sample"] = "full objective on this grid (restatement, own cache)"
         else:
             # bounded sample: a 21 x 400 grid, scaled by S^2
             sn = 21 * 400
             t0 = time.time()
-            port.objective(21, 400, bs, Cfg(*STATIC[:8], STATIC[8]), fh[:sn], 5, threads=threads)
+            _cpu_objective(port, 21, 400, bs, fh[:sn], threads)
             dt = time.time() - t0
             rec["cpu_objective_s"] = dt * (n / sn) ** 2
             rec["cpu_sample"] = f"21x400 grid ({sn} tokens) timed {dt:.2f} s, scaled by (S/{sn})^2"

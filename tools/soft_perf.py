@@ -12,6 +12,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+from bench import ClockSampler  # noqa: E402
 from paper_2604_20470_b200 import radialplan as rp  # noqa: E402
 
 
@@ -32,21 +33,23 @@ def main():
     g = rp.make_grid(nf, nt, 128)
     cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(1.0, 0.1), 1.0, 0.2, 0.3, 0.3)
     mask = rp.Plan(g, cfg, 7).build_mask_device()
-    gen = torch.Generator(device="cuda").manual_seed(42)
-    q, k, v = (torch.randn(nf * nt, H, d, device="cuda", generator=gen).to(torch.bfloat16)
-               for _ in range(3))
+    fb = rp.random_batch(nf * nt, H, d, 42)
+    q, k, v = fb.queries, fb.keys, fb.values
     out = torch.empty((g.padded_tokens, H, d), dtype=torch.bfloat16, device="cuda")
     rpt, col, order = rp.mask_to_csr(g, mask)
-    exact = timed(lambda: rp.sparse_attention(g, q, k, v, rpt, col, order, out=out))
-    soft = timed(lambda: rp.soft_attention(g, q, k, v, mask, 1e-10, out=out))
-    qs, ks, vs = (x.permute(1, 0, 2).unsqueeze(0) for x in (q, k, v))
-    sdpa = timed(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs))
+    with ClockSampler(0) as clk:
+        exact = timed(lambda: rp.sparse_attention(g, q, k, v, rpt, col, order, out=out))
+        soft = timed(lambda: rp.soft_attention(g, q, k, v, mask, 1e-10, out=out))
+        qs, ks, vs = (x.permute(1, 0, 2).unsqueeze(0) for x in (q, k, v))
+        sdpa = timed(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs))
     nb = g.blocks_per_dim
     flop = 4.0 * H * d * 128 * 128 * nb * nb
     rec = {"workload": "Wan2.1 21x3600, 40 heads, d=128, bf16, config-3 static mask",
            "exact_sparse_ms": exact, "soft_mask_ms": soft, "sdpa_dense_ms": sdpa,
            "soft_tflops": flop / (soft * 1e-3) / 1e12,
-           "soft_vs_sdpa_dense": sdpa / soft}
+           "soft_vs_sdpa_dense": sdpa / soft, "clocks": clk.summary(),
+           "kernel_soft": "dense row lists + per-block log-eps offset on "
+                          + rp.attention_kernel(g, "bf16", d)}
     print(json.dumps(rec))
     if len(sys.argv) > 1:
         with open(sys.argv[1], "w") as f:
