@@ -44,15 +44,29 @@
 namespace rp {
 namespace mask {
 
-struct ScoreItem {
-  int32_t job;    // index into the engine's job array
-  int32_t tr;     // 128-token tile row (global)
-  int32_t tc;     // 128-token tile column (global)
-  int32_t width;  // the job's band half-width (copied: one load per item)
-  int32_t qi;     // first token of frame i
-  int32_t kj;     // first token of frame j
-  int32_t pad0, pad1;
+// Everything the epilogue needs about one 128 x 128 item, precomputed on the
+// host so an item costs three 16-byte loads and 32-bit index math only.
+struct alignas(16) ScoreItem {
+  int32_t job;       // index into the engine's job array
+  int32_t tr;        // 128-token tile row (global)
+  int32_t tc;        // 128-token tile column (global)
+  int32_t width;     // the job's band half-width, clamped to N_t
+  int32_t u0, v0;    // tr * 128 - first token of frame i, tc * 128 - first of frame j
+  int32_t rr0, cc0;  // the tile's first block row / column in the job's count rectangle
+  int32_t jtr, jtc;  // the job's count rectangle (block rows / columns)
+  long long cnt_off; // the job's [tr][tc][B] count offset
 };
+static_assert(sizeof(ScoreItem) == 48, "ScoreItem is loaded as three int4");
+
+RP_DEV ScoreItem load_item(const ScoreItem* items, long long i) {
+  const int4* src = reinterpret_cast<const int4*>(items + i);
+  ScoreItem x;
+  int4* dst = reinterpret_cast<int4*>(&x);
+  dst[0] = __ldg(src);
+  dst[1] = __ldg(src + 1);
+  dst[2] = __ldg(src + 2);
+  return x;
+}
 
 struct SParams {
   const DJob* jobs;
@@ -60,7 +74,8 @@ struct SParams {
   long long n_items;
   const int2* units;  // [n_units] item ranges [x, y), see UnitCursor
   int n_units;
-  int nt, bs, cph;       // tokens per frame, block size, 64-wide chunks per head
+  int nt, bs, lg_bs, cph;  // tokens per frame, block size (32/64/128) and its log2,
+                           // 64-wide chunks per head
   float score_scale;     // inv_sqrt_d / H_f
   double* item_stats;    // pass 1: [n_items][3] (n, mean, M2)
   const double2* job_stats;  // pass 2: mean, stddev per job
@@ -129,9 +144,8 @@ RP_DEV Welford chan(Welford a, Welford b) {
 
 // Overflowing undecided pair: decided here with the exact fp64 score.  Out
 // of line so the epilogue's unrolled loops stay compact.
-__device__ __noinline__ bool decide_exact(const SParams& p, const DJob& jb, int v, long long gr,
-                                          long long kj, double2 st) {
-  return zscore(exact_score(p.feat, gr, kj + v), st) >= jb.param;
+__device__ __noinline__ bool decide_exact(const SParams& p, int job, long long gr, long long gc) {
+  return zscore(exact_score(p.feat, gr, gc), p.job_stats[job]) >= p.jobs[job].param;
 }
 
 // Work order: units (one frame pair's items of one 128-token tile row, so
@@ -289,42 +303,38 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
     // pass-2 threshold, |q'| of the row, max |k'| of the tile) one item
     // later, so no global-load latency sits on an item's critical path.
     ScoreItem itm0{}, itm1{};
-    DJob jb0{};
     float2 thr0 = make_float2(0.f, 0.f);
     float qn0 = 0.f, km0 = 0.f;
     auto job_loads = [&](const ScoreItem& x) {
-      jb0 = p.jobs[x.job];
       if (MODE == 1) {
-        thr0 = p.job_thr[x.job];
-        qn0 = __ldg(p.qnorm + static_cast<long long>(x.tr) * 128 + r);
+        thr0 = __ldg(p.job_thr + x.job);
+        qn0 = __ldg(p.qnorm + x.tr * 128 + r);
         km0 = __ldg(p.kmax + x.tc);
       }
     };
     UnitCursor ahead(p);
     if (ahead.valid()) {
-      itm0 = p.items[ahead.it];
+      itm0 = load_item(p.items, ahead.it);
       job_loads(itm0);
       ahead.next();
     }
     bool has1 = ahead.valid();
     if (has1) {
-      itm1 = p.items[ahead.it];
+      itm1 = load_item(p.items, ahead.it);
       ahead.next();
     }
     for (UnitCursor cur(p); cur.valid(); cur.next(), ++n) {
       const long long it = cur.it;
       const ScoreItem item = itm0;
-      const DJob jb = jb0;
       const float2 thr = thr0;
       const float qk = qn0 * p.kappa * km0;
       if (has1) job_loads(itm1);
       itm0 = itm1;
       has1 = ahead.valid();
       if (has1) {
-        itm1 = p.items[ahead.it];
+        itm1 = load_item(p.items, ahead.it);
         ahead.next();
       }
-      const long long gr = static_cast<long long>(item.tr) * 128 + r;
       const uint32_t buf = n & 1;
       mbar_wait(&s_full[buf], (n >> 1) & 1);
       tc_fence_after();
@@ -340,15 +350,11 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
       continue;
 #endif
       // valid columns of this row: contiguous [c_lo, c_hi] (band + frames)
-      const long long qi = item.qi;
-      const long long kj = item.kj;
-      const long long u = gr - qi;
+      const int u = item.u0 + r;  // row within frame i
       int c_lo = 1, c_hi = 0;
       if (u >= 0 && u < p.nt) {
-        const long long vlo = max(0ll, u - item.width), vhi = min(static_cast<long long>(p.nt) - 1, u + item.width);
-        const long long g0 = static_cast<long long>(item.tc) * 128;
-        c_lo = static_cast<int>(max(kj + vlo - g0, 0ll));
-        c_hi = static_cast<int>(min(kj + vhi - g0, 127ll));
+        c_lo = max(max(u - item.width, 0) - item.v0, 0);
+        c_hi = min(min(u + item.width, p.nt - 1) - item.v0, 127);
       }
       uint32_t inm[NW];
       int cnt = 0;
@@ -444,37 +450,43 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
         int mine = 0;
 #pragma unroll
         for (int w4 = 0; w4 < NW; ++w4) mine += __popc(ub[w4]);
-        int incl = mine;
+        uint8_t* scnt = p.slot_cnt + it * E::kWarps + warp;
+        if (__any_sync(0xFFFFFFFFu, mine != 0)) {
+          int incl = mine;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const long long sbase = it * kSlotsPerItem + warp * E::kSlots;
-        if (lane == 0) p.slot_cnt[it * E::kWarps + warp] = static_cast<uint8_t>(min(total, E::kSlots));
-        if (mine) {
-          int at = incl - mine;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+          const long long sbase = it * kSlotsPerItem + warp * E::kSlots;
+          if (lane == 0) *scnt = static_cast<uint8_t>(min(total, E::kSlots));
+          if (mine) {
+            int at = incl - mine;
 #pragma unroll
-          for (int w4 = 0; w4 < NW; ++w4) {
-            uint32_t m = ub[w4];
-            while (m) {
-              const int i = __ffs(m) - 1;
-              m &= m - 1;
-              const int v = static_cast<int>(static_cast<long long>(item.tc) * 128 +
-                                             32 * (cg * NW + w4) + i - kj);
-              if (at < E::kSlots)
-                p.slots[sbase + at] = make_uint2(static_cast<uint32_t>(item.job),
-                                                 static_cast<uint32_t>(u) * p.nt + v);
-              else if (decide_exact(p, jb, v, gr, kj, p.job_stats[item.job]))
-                kb[w4] |= 1u << i;
-              ++at;
+            for (int w4 = 0; w4 < NW; ++w4) {
+              uint32_t m = ub[w4];
+              while (m) {
+                const int i = __ffs(m) - 1;
+                m &= m - 1;
+                const int v = item.v0 + 32 * (cg * NW + w4) + i;
+                if (at < E::kSlots)
+                  p.slots[sbase + at] = make_uint2(static_cast<uint32_t>(item.job),
+                                                   static_cast<uint32_t>(u) * p.nt + v);
+                else if (decide_exact(p, item.job, static_cast<long long>(item.tr) * 128 + r,
+                                      static_cast<long long>(item.tc) * 128 +
+                                          32 * (cg * NW + w4) + i))
+                  kb[w4] |= 1u << i;
+                ++at;
+              }
             }
           }
+        } else if (lane == 0) {
+          *scnt = 0;
         }
         // per-column counts within the warp: transpose each 32 x 32 bit block
         // (lane = row -> lane = column) and count
-        unsigned long long kept_total = 0;
+        unsigned kept_total = 0;
 #pragma unroll
         for (int w4 = 0; w4 < NW; ++w4) {
           uint32_t x = kb[w4];
@@ -489,25 +501,25 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
           wcnt_base[(n & 1) * 512 + rw * 128 + (cg * NW + w4) * 32 + lane] = __popc(x);
         }
         epi_bar<CG>();
-        // thread et < 128 owns column et: sum the row groups of each block row
-        const int bs = p.bs;
-        const int rows_per_blk = bs < 128 ? bs : 128;  // bs in {32, 64, 128}
-        const int wpb = rows_per_blk >> 5;             // row groups per block row
+        // thread et < 128 owns column et: sum the row groups of each block
+        // row (bs = 32 << k: 128 / bs block rows of bs / 32 row groups)
         if (et < 128) {
-          const long long gc = static_cast<long long>(item.tc) * 128 + et;
-          for (int br = 0; br < 4 / wpb; ++br) {
-            uint32_t c2 = 0;
-            for (int x = 0; x < wpb; ++x) c2 += wcnt_base[(n & 1) * 512 + (br * wpb + x) * 128 + et];
-            const long long R = (static_cast<long long>(item.tr) * 128) / bs + br;
-            const long long Cb = gc / bs;
-            const long long rr = R - jb.r0, cc = Cb - jb.c0;
-            if (rr >= 0 && rr < jb.tr && cc >= 0 && cc < jb.tc && c2)
-              p.counts[jb.cnt_off + (rr * jb.tc + cc) * bs + gc % bs] = c2;
+          const int lg = p.lg_bs;
+          const int cc = item.cc0 + (et >> lg);
+          if (cc >= 0 && cc < item.jtc) {
+            const int wpb = p.bs >> 5;
+            const int within = et & (p.bs - 1);
+            for (int br = 0; br < (128 >> lg); ++br) {
+              uint32_t c2 = 0;
+              for (int x = 0; x < wpb; ++x) c2 += wcnt_base[(n & 1) * 512 + (br * wpb + x) * 128 + et];
+              const int rr = item.rr0 + br;
+              if (rr >= 0 && rr < item.jtr && c2)
+                p.counts[item.cnt_off + (static_cast<long long>(rr * item.jtc + cc) << lg) + within] = c2;
+            }
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) kept_total += __shfl_xor_sync(0xFFFFFFFFu, kept_total, o);
-        if (lane == 0 && kept_total) atomicAdd(&p.job_kept[item.job], kept_total);
+        kept_total = __reduce_add_sync(0xFFFFFFFFu, kept_total);
+        if (lane == 0 && kept_total) atomicAdd(&p.job_kept[item.job], static_cast<unsigned long long>(kept_total));
         // no trailing barrier (wcnt is double-buffered, see red above)
       }
     }
@@ -762,9 +774,19 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
         const int64_t va = std::max<int64_t>(tc * 128, kj) - kj;
         const int64_t vb = std::min<int64_t>(tc * 128 + 127, kj + nt - 1) - kj;
         if (va - ub > d.width || ua - vb > d.width) continue;  // no |u - v| <= w
-        e->items.push_back(ScoreItem{job, static_cast<int32_t>(tr), static_cast<int32_t>(tc),
-                                     static_cast<int32_t>(d.width), static_cast<int32_t>(qi),
-                                     static_cast<int32_t>(kj), 0, 0});
+        ScoreItem x{};
+        x.job = job;
+        x.tr = static_cast<int32_t>(tr);
+        x.tc = static_cast<int32_t>(tc);
+        x.width = static_cast<int32_t>(std::min<int64_t>(d.width, nt));
+        x.u0 = static_cast<int32_t>(tr * 128 - qi);
+        x.v0 = static_cast<int32_t>(tc * 128 - kj);
+        x.rr0 = static_cast<int32_t>(tr * 128 / bs - d.r0);
+        x.cc0 = static_cast<int32_t>(tc * 128 / bs - d.c0);
+        x.jtr = d.tr;
+        x.jtc = d.tc;
+        x.cnt_off = d.cnt_off;
+        e->items.push_back(x);
       }
     }
     for (int32_t r = 0; r < d.tr; ++r)
@@ -903,6 +925,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.n_units = static_cast<int>(e->units.size());
   p.nt = g.tokens_per_frame;
   p.bs = g.block_size;
+  p.lg_bs = g.block_size == 32 ? 5 : g.block_size == 64 ? 6 : 7;
   p.cph = e->dim / 64;
   p.score_scale = static_cast<float>((1.0 / std::sqrt(static_cast<double>(e->dim))) / e->heads);
   p.item_stats = e->d_item_stats;
