@@ -155,15 +155,16 @@ __device__ __noinline__ bool decide_exact(const SParams& p, int job, long long g
 // tiles come from L2 instead of HBM.
 struct UnitCursor {
   const int2* units;
-  int n, u, it, hi;
+  int n, u, it, lo, hi;
   RP_DEV explicit UnitCursor(const SParams& p)
-      : units(p.units), n(p.n_units), u(static_cast<int>(blockIdx.x)), it(0), hi(0) {
+      : units(p.units), n(p.n_units), u(static_cast<int>(blockIdx.x)), it(0), lo(0), hi(0) {
     load();
   }
   RP_DEV void load() {
     if (u < n) {
       const int2 x = units[u];
       it = x.x;
+      lo = x.x;
       hi = x.y;
     }
   }
@@ -298,6 +299,9 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
     const int et = warp * 32 + lane;          // epilogue thread index
     const uint32_t trow = tmem + (static_cast<uint32_t>(rw * 32) << 16) + cg * 32 * NW;
     uint32_t n = 0;
+    double u1 = 0.0, u2 = 0.0;  // pass 1: this row's sums over the current unit
+    int un = 0;
+    uint32_t nu = 0;  // units reduced (red[] parity)
     // Item metadata is software-pipelined: item n + 2 is loaded while item n
     // is processed, and the loads that depend on it (its frame pair, the
     // pass-2 threshold, |q'| of the row, max |k'| of the tile) one item
@@ -381,36 +385,48 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
             a2[i & 3] = fmaf(x, x, a2[i & 3]);
           }
         }
-        double t1 = static_cast<double>((a1[0] + a1[1]) + (a1[2] + a1[3]));
-        double t2 = static_cast<double>((a2[0] + a2[1]) + (a2[2] + a2[3]));
-        double tn = static_cast<double>(cnt);
+        // the row's sums are carried in fp64 across the items of the unit
+        // (one frame pair, one tile row) and reduced once per unit: the
+        // unit's stats go to its first item, the others keep n = 0 (zeroed
+        // before the pass), which the per-job Chan merge skips
+        u1 += static_cast<double>((a1[0] + a1[1]) + (a1[2] + a1[3]));
+        u2 += static_cast<double>((a2[0] + a2[1]) + (a2[2] + a2[3]));
+        un += cnt;
+        if (it + 1 == cur.hi) {
+          const int tn = __reduce_add_sync(0xFFFFFFFFu, un);
+          double t1 = u1, t2 = u2;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly -> deterministic lane 0
-          t1 += __shfl_xor_sync(0xFFFFFFFFu, t1, o);
-          t2 += __shfl_xor_sync(0xFFFFFFFFu, t2, o);
-          tn += __shfl_xor_sync(0xFFFFFFFFu, tn, o);
-        }
-        double* red = red_base + (n & 1) * 16 * 3;
-        if (lane == 0) {
-          red[warp * 3 + 0] = tn;
-          red[warp * 3 + 1] = t1;
-          red[warp * 3 + 2] = t2;
-        }
-        epi_bar<CG>();
-        if (et == 0) {
-          double N = 0.0, S1 = 0.0, S2 = 0.0;
-          for (int x = 0; x < E::kWarps; ++x) {
-            N += red[3 * x];
-            S1 += red[3 * x + 1];
-            S2 += red[3 * x + 2];
+          for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly -> deterministic lane 0
+            t1 += __shfl_xor_sync(0xFFFFFFFFu, t1, o);
+            t2 += __shfl_xor_sync(0xFFFFFFFFu, t2, o);
           }
-          const double mean = N > 0.0 ? S1 / N : 0.0;
-          p.item_stats[3 * it + 0] = N;
-          p.item_stats[3 * it + 1] = mean;
-          p.item_stats[3 * it + 2] = N > 0.0 ? fmax(S2 - S1 * mean, 0.0) : 0.0;
+          double* red = red_base + (nu & 1) * 16 * 3;
+          if (lane == 0) {
+            red[warp * 3 + 0] = static_cast<double>(tn);
+            red[warp * 3 + 1] = t1;
+            red[warp * 3 + 2] = t2;
+          }
+          epi_bar<CG>();
+          if (et == 0) {
+            double N = 0.0, S1 = 0.0, S2 = 0.0;
+            for (int x = 0; x < E::kWarps; ++x) {
+              N += red[3 * x];
+              S1 += red[3 * x + 1];
+              S2 += red[3 * x + 2];
+            }
+            const double mean = N > 0.0 ? S1 / N : 0.0;
+            const long long first = cur.lo;
+            p.item_stats[3 * first + 0] = N;
+            p.item_stats[3 * first + 1] = mean;
+            p.item_stats[3 * first + 2] = N > 0.0 ? fmax(S2 - S1 * mean, 0.0) : 0.0;
+          }
+          // no trailing barrier: the next unit writes the other red buffer,
+          // and this one is rewritten only after the next unit's barrier
+          u1 = 0.0;
+          u2 = 0.0;
+          un = 0;
+          ++nu;
         }
-        // no trailing barrier: the next item writes the other red buffer, and
-        // this one is rewritten only after the next item's barrier
       } else {
         // Decision thresholds of this row in raw accumulator units.  The
         // fast score differs from the reference's by at most
@@ -950,6 +966,8 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   for (int mode = 0; mode < 2; ++mode) {
     const int st = mode == 0 ? kStageScoreStats : kStageScoreSelect;
     stage_begin(st, s);
+    if (mode == 0)  // per-unit stats land on each unit's first item
+      RP_CUDA(cudaMemsetAsync(e->d_item_stats, 0, sizeof(double) * 3 * e->items.size(), s));
     switch (e->nc) {
       case 1: launch_pass<1>(mq, mk, p, mode, grid, s); break;
       case 2: launch_pass<2>(mq, mk, p, mode, grid, s); break;
