@@ -82,18 +82,18 @@ struct SParams {
   const float2* job_thr;     // pass 2: (raw-unit threshold, raw-unit delta margin) per job
   uint32_t* counts;
   unsigned long long* job_kept;
-  uint2* slots;          // [n_items][epilogue warps][slots]: (job, u * nt + v) to re-score
-  uint8_t* slot_cnt;     // [n_items][epilogue warps]
+  uint2* upairs;       // undecided pairs (job, u * nt + v): one region of ucap per CTA
+  unsigned ucap;       // region capacity (pairs beyond it are decided in place)
+  unsigned* ucount;    // [grid] pairs in each CTA's region
   const float* qnorm;
   const float* kmax;  // per 128-token tile: max |k'_v|
   float kappa;
   float delta_floor;
-  Feat feat;  // exact re-score in place when a warp's slots overflow
+  Feat feat;  // exact re-score in place when the undecided list is full
 };
 
-// Undecided pairs per (item, epilogue warp) kept for the exact re-score
-// without any global atomics; more than this (never seen in practice: the
-// mean is < 1 per warp) are decided in place.
+// Capacity of the undecided-pair list per item (the mean at the Hunyuan
+// shape is ~3.4 per item); pairs beyond it are decided in place.
 #ifndef RP_SCORE_ABL
 #define RP_SCORE_ABL 0
 #endif
@@ -108,7 +108,6 @@ struct Epi {
   static constexpr int kWarps = 4 * CG;
   static constexpr int kThreads = 32 * (kWarps + 2);
   static constexpr int kNW = 4 / CG;                    // 32-column words per warp
-  static constexpr int kSlots = kSlotsPerItem / kWarps;  // recheck slots per warp
 };
 constexpr int kChunkBytes = 128 * 128;
 
@@ -118,7 +117,8 @@ struct SLayout {
   static constexpr int kStages = 2;
   static constexpr int kSmemData = (1 + kStages) * kTileBytes;
   static constexpr int kNumBars = 2 * kStages + 6;
-  // bars | tmem slot (16 B) | (unused 512 B) | wcnt[2][4][128] | red[2][16][3] doubles
+  // bars | tmem slot (16 B) | 512 B (word 0: undecided-pair counter) | wcnt[2][4][128] |
+  // red[2][16][3] doubles
   // (wcnt / red double-buffered by item parity: one epilogue barrier per item)
   static constexpr int kExtra = kNumBars * 8 + 16 + 128 * 4 + 2 * 4 * 128 * 4 + 2 * 16 * 3 * 8;
   static constexpr int kSmemBytes = kSmemData + kExtra + 1024;
@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
   uint64_t* s_full = q_full + 2;   // [2]
   uint64_t* s_empty = q_full + 4;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::kNumBars);
+  unsigned* s_ucnt = tmem_slot + 4;  // pass 2: pairs in this CTA's undecided region
   uint32_t* wcnt_base = reinterpret_cast<uint32_t*>(tmem_slot + 4 + 128);  // [2][4][128]
   double* red_base = reinterpret_cast<double*>(wcnt_base + 2 * 4 * 128);  // [2][16][3]
 
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
     }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
+    *s_ucnt = 0;
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&s_empty[b], E::kWarps);
@@ -461,12 +463,11 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
           kb[w4] = k1 & inm[w4];
           ub[w4] = u1 & inm[w4] & ~k1;
         }
-        // rare path: undecided pairs go to this (item, warp)'s slots for the
-        // exact fp64 re-score (warp scan for the slot offsets, no atomics)
+        // rare path: undecided pairs are appended to one compact list for the
+        // exact fp64 re-score (one atomic per warp, warp scan for the offsets)
         int mine = 0;
 #pragma unroll
         for (int w4 = 0; w4 < NW; ++w4) mine += __popc(ub[w4]);
-        uint8_t* scnt = p.slot_cnt + it * E::kWarps + warp;
         if (__any_sync(0xFFFFFFFFu, mine != 0)) {
           int incl = mine;
 #pragma unroll
@@ -474,11 +475,11 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
             const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
             if (lane >= o) incl += y;
           }
-          const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-          const long long sbase = it * kSlotsPerItem + warp * E::kSlots;
-          if (lane == 0) *scnt = static_cast<uint8_t>(min(total, E::kSlots));
+          unsigned base = 0;
+          if (lane == 31) base = atomicAdd(s_ucnt, static_cast<unsigned>(incl));
+          base = __shfl_sync(0xFFFFFFFFu, base, 31);
           if (mine) {
-            int at = incl - mine;
+            unsigned at = base + static_cast<unsigned>(incl - mine);
 #pragma unroll
             for (int w4 = 0; w4 < NW; ++w4) {
               uint32_t m = ub[w4];
@@ -486,9 +487,9 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
                 const int i = __ffs(m) - 1;
                 m &= m - 1;
                 const int v = item.v0 + 32 * (cg * NW + w4) + i;
-                if (at < E::kSlots)
-                  p.slots[sbase + at] = make_uint2(static_cast<uint32_t>(item.job),
-                                                   static_cast<uint32_t>(u) * p.nt + v);
+                if (at < p.ucap)
+                  p.upairs[static_cast<long long>(blockIdx.x) * p.ucap + at] = make_uint2(static_cast<uint32_t>(item.job),
+                                            static_cast<uint32_t>(u) * p.nt + v);
                 else if (decide_exact(p, item.job, static_cast<long long>(item.tr) * 128 + r,
                                       static_cast<long long>(item.tc) * 128 +
                                           32 * (cg * NW + w4) + i))
@@ -497,8 +498,6 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
               }
             }
           }
-        } else if (lane == 0) {
-          *scnt = 0;
         }
         // per-column counts within the warp: transpose each 32 x 32 bit block
         // (lane = row -> lane = column) and count
@@ -543,6 +542,7 @@ __global__ void __launch_bounds__(Epi<CG>::kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (MODE == 1 && threadIdx.x == 0) p.ucount[blockIdx.x] = *s_ucnt;
   if (warp == kMma) {
     tc_fence_after();
     tmem_dealloc<256>(tmem);
@@ -604,28 +604,29 @@ __global__ void tile_max_kernel(const float* __restrict__ norms, long long token
 
 // Exact re-score of every undecided pair (reference operation order): one
 // thread per (item, warp) slot group.
-__global__ void recheck_kernel(const DJob* __restrict__ jobs, const uint2* __restrict__ slots,
-                               const uint8_t* __restrict__ slot_cnt, long long groups, Feat f,
+// blockIdx.y = the scoring CTA whose undecided region this block walks.
+__global__ void recheck_kernel(const DJob* __restrict__ jobs, const uint2* __restrict__ upairs,
+                               const unsigned* __restrict__ ucount, unsigned ucap, Feat f,
                                const double2* __restrict__ job_stats, uint32_t* counts,
                                unsigned long long* job_kept, unsigned long long* rechecked,
-                               int nt, int bs, int slots_per_group) {
-  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < groups;
-       x += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int n = slot_cnt[x];
-    if (!n) continue;
-    atomicAdd(rechecked, static_cast<unsigned long long>(n));
-    for (int e = 0; e < n; ++e) {
-      const uint2 sl = slots[x * slots_per_group + e];
-      const DJob& jb = jobs[sl.x];
-      const int64_t u = sl.y / nt, v = sl.y % nt;
-      const float s = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
-                                  static_cast<int64_t>(jb.j) * nt + v);
-      if (zscore(s, job_stats[sl.x]) >= jb.param) {
-        add_count(jb, counts, nt, bs, u, v);
-        atomicAdd(&job_kept[sl.x], 1ull);
-      }
+                               int nt, int bs) {
+  const unsigned n = min(ucount[blockIdx.y], ucap);
+  upairs += static_cast<long long>(blockIdx.y) * ucap;
+  unsigned done = 0;
+  for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const uint2 sl = upairs[x];
+    const DJob& jb = jobs[sl.x];
+    const int64_t u = sl.y / nt, v = sl.y % nt;
+    const float sc = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
+                                 static_cast<int64_t>(jb.j) * nt + v);
+    if (zscore(sc, job_stats[sl.x]) >= jb.param) {
+      add_count(jb, counts, nt, bs, u, v);
+      atomicAdd(&job_kept[sl.x], 1ull);
     }
+    ++done;
   }
+  done = __reduce_add_sync(0xFFFFFFFFu, done);
+  if ((threadIdx.x & 31) == 0 && done) atomicAdd(rechecked, static_cast<unsigned long long>(done));
 }
 
 // Exact fallback for frame pairs that kept nothing: exact scores of the
@@ -723,8 +724,8 @@ class FastEngine {
   double2* d_job_stats = nullptr;
   float2* d_job_thr = nullptr;
   unsigned long long* d_kept = nullptr;  // [jobs + 1]: per job, then rechecked pairs
-  uint2* d_slots = nullptr;
-  uint8_t* d_slot_cnt = nullptr;
+  uint2* d_upairs = nullptr;
+  unsigned* d_ucount = nullptr;
   float* d_qn = nullptr;
   float* d_kn = nullptr;
   float* d_kmax = nullptr;
@@ -736,7 +737,7 @@ class FastEngine {
                     static_cast<void*>(d_counts), static_cast<void*>(d_item_stats),
                     static_cast<void*>(d_job_stats), static_cast<void*>(d_kept),
                     static_cast<void*>(d_job_thr),
-                    static_cast<void*>(d_slots), static_cast<void*>(d_slot_cnt),
+                    static_cast<void*>(d_upairs), static_cast<void*>(d_ucount),
                     static_cast<void*>(d_qn),
                     static_cast<void*>(d_kn), static_cast<void*>(d_kmax)})
       if (p) cudaFree(p);
@@ -846,8 +847,8 @@ FastEngine* fast_engine_create(const rp_grid& g, const std::vector<DJob>& all, i
   dalloc(&e->d_job_stats, nj);
   dalloc(&e->d_job_thr, nj);
   dalloc(&e->d_kept, nj + 1);
-  dalloc(&e->d_slots, e->items.size() * kSlotsPerItem);
-  dalloc(&e->d_slot_cnt, e->items.size() * 16);  // up to 16 epilogue warps
+  dalloc(&e->d_upairs, e->items.size() * kSlotsPerItem);
+  dalloc(&e->d_ucount, 1024);  // one per scoring CTA (grid <= SM count)
   dalloc(&e->d_qn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kn, static_cast<size_t>(g.padded_tokens));
   dalloc(&e->d_kmax, static_cast<size_t>((g.padded_tokens + 127) / 128));
@@ -949,8 +950,8 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.job_thr = e->d_job_thr;
   p.counts = e->d_counts;
   p.job_kept = e->d_kept;
-  p.slots = e->d_slots;
-  p.slot_cnt = e->d_slot_cnt;
+  p.upairs = e->d_upairs;
+  p.ucount = e->d_ucount;
   p.qnorm = e->d_qn;
   p.kmax = e->d_kmax;
   // fp32 accumulation of K = H_f * d exact bf16 products, each rounding
@@ -962,7 +963,10 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   int dev = 0, sms = 0;
   RP_CUDA(cudaGetDevice(&dev));
   RP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::min(p.n_units, sms);
+  const int grid = std::min(p.n_units, std::min(sms, 1024));
+  p.ucap = static_cast<unsigned>(
+      std::min<long long>(static_cast<long long>(e->items.size()) * kSlotsPerItem / grid,
+                          0x7fffffffLL));
   for (int mode = 0; mode < 2; ++mode) {
     const int st = mode == 0 ? kStageScoreStats : kStageScoreSelect;
     stage_begin(st, s);
@@ -987,12 +991,9 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   // exact re-score of the pairs within their error bound of tau
   stage_begin(kStageRecheck, s);
   {
-    const int ew = 4 * score_cg(1);  // slots are written by the select pass
-    const long long groups = static_cast<long long>(e->items.size()) * ew;
-    recheck_kernel<<<static_cast<unsigned>(std::min<long long>((groups + 255) / 256, sms * 16)),
-                     256, 0, s>>>(e->d_jobs, e->d_slots, e->d_slot_cnt, groups, f,
-                                  e->d_job_stats, e->d_counts, e->d_kept, e->d_kept + nj,
-                                  g.tokens_per_frame, g.block_size, kSlotsPerItem / ew);
+    recheck_kernel<<<dim3(8, static_cast<unsigned>(grid)), 256, 0, s>>>(
+        e->d_jobs, e->d_upairs, e->d_ucount, p.ucap, f, e->d_job_stats, e->d_counts, e->d_kept,
+        e->d_kept + nj, g.tokens_per_frame, g.block_size);
     RP_LAUNCHED();
   }
   // fallback_k: only when it can activate a column (fallback_k >= cmin)
