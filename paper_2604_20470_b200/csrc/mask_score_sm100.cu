@@ -567,23 +567,61 @@ __global__ void norm_kernel(const __nv_bfloat16* __restrict__ x, long long token
   if (lane == 0) out[t] = sqrtf(acc);
 }
 
-// Deterministic per-frame-pair merge of item statistics (fixed item order).
+// Deterministic per-frame-pair merge of item statistics: one warp per job,
+// lane l Chan-merges items l, l + 32, ... (only each unit's first item
+// carries stats), then a fixed butterfly.
 __global__ void job_stats_kernel(const double* __restrict__ item_stats,
                                  const long long* __restrict__ job_item_off, int n_jobs,
                                  const DJob* __restrict__ jobs, double score_scale,
                                  double delta_floor, double2* __restrict__ job_stats,
                                  float2* __restrict__ job_thr) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = static_cast<int>((blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (j >= n_jobs) return;
   Welford a{0.0, 0.0, 0.0};
-  for (long long it = job_item_off[j]; it < job_item_off[j + 1]; ++it)
+  for (long long it = job_item_off[j] + lane; it < job_item_off[j + 1]; it += 32)
     a = chan(a, Welford{item_stats[3 * it], item_stats[3 * it + 1], item_stats[3 * it + 2]});
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Welford b;
+    b.n = __shfl_xor_sync(0xFFFFFFFFu, a.n, o);
+    b.mean = __shfl_xor_sync(0xFFFFFFFFu, a.mean, o);
+    b.m2 = __shfl_xor_sync(0xFFFFFFFFu, a.m2, o);
+    a = (lane & o) ? chan(b, a) : chan(a, b);  // lower lanes' items first on both sides
+  }
+  if (lane != 0) return;
   const double sd = a.n > 0 ? sqrt(a.m2 / a.n) : 0.0;
   job_stats[j] = make_double2(a.mean, sd);
   // pass-2 thresholds in raw accumulator units (see score_kernel)
   const double tau = jobs[j].param, sde = sd + 1e-8;
   job_thr[j] = make_float2(__double2float_rn((tau * sde + a.mean) / score_scale),
                            __double2float_ru(delta_floor * (2.0 + fabs(tau)) * sde / score_scale));
+}
+
+// theta_c / theta_m per block tile from the count buffer (mask.cpp:87-125,
+// as apply_kernel mode 1): one warp per tile, bs / 32 columns per lane.
+__global__ void apply_tiles_kernel(const DJob* __restrict__ jobs, const Item* __restrict__ tiles,
+                                   long long n_tiles, const uint32_t* __restrict__ counts,
+                                   uint32_t* words, int bs, int64_t row_bytes, uint32_t cmin,
+                                   int amin) {
+  const long long t = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= n_tiles) return;
+  const Item it = tiles[t];
+  const DJob& jb = jobs[it.job];
+  const uint32_t* c = counts + jb.cnt_off + (static_cast<int64_t>(it.tr) * jb.tc + it.tc) * bs;
+  int mine;
+  if (bs == 128) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(c) + lane);
+    mine = (v.x >= cmin) + (v.y >= cmin) + (v.z >= cmin) + (v.w >= cmin);
+  } else if (bs == 64) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(c) + lane);
+    mine = (v.x >= cmin) + (v.y >= cmin);
+  } else {
+    mine = __ldg(c + lane) >= cmin;
+  }
+  const int active = __reduce_add_sync(0xFFFFFFFFu, mine);
+  if (lane == 0 && active >= amin) set_block(words, row_bytes, jb.r0 + it.tr, jb.c0 + it.tc);
 }
 
 // Max of the per-token norms over each 128-token tile (one warp per tile).
@@ -981,7 +1019,7 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
     stage_end(st, s);
     if (mode == 0) {
       stage_begin(kStageJobStats, s);
-      job_stats_kernel<<<(nj + 127) / 128, 128, 0, s>>>(e->d_item_stats, e->d_job_item_off, nj,
+      job_stats_kernel<<<(nj + 7) / 8, 256, 0, s>>>(e->d_item_stats, e->d_job_item_off, nj,
                                                        e->d_jobs, p.score_scale, delta_floor,
                                                        e->d_job_stats, e->d_job_thr);
       RP_LAUNCHED();
@@ -1023,14 +1061,11 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   stage_end(kStageRecheck, s);
   // theta_c / theta_m per block tile of every scored frame pair
   stage_begin(kStageApply, s);
-  const int64_t chunk = int64_t{1} << 30;
-  for (int64_t b = 0; b < static_cast<int64_t>(e->tiles.size()); b += chunk) {
-    const int64_t n = std::min<int64_t>(chunk, e->tiles.size() - b);
-    const int th = g.block_size >= 1024 ? 1024 : (g.block_size < 32 ? 32 : g.block_size);
-    apply_kernel<<<static_cast<unsigned>(n), th, 0, s>>>(e->d_jobs, e->d_tiles + b, e->d_counts,
-                                                         words, g.tokens_per_frame,
-                                                         g.block_size, g.row_bytes, e->cmin,
-                                                         e->amin, 1);
+  {
+    const long long nt_ = static_cast<long long>(e->tiles.size());
+    apply_tiles_kernel<<<static_cast<unsigned>((nt_ + 7) / 8), 256, 0, s>>>(
+        e->d_jobs, e->d_tiles, nt_, e->d_counts, words, g.block_size, g.row_bytes,
+        static_cast<uint32_t>(e->cmin), e->amin);
     RP_LAUNCHED();
   }
   stage_end(kStageApply, s);

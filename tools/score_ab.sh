@@ -9,5 +9,5 @@ done
 for v in new $1; do
   echo "== ncu $v"
   if [ $v = new ]; then L=; else L=DYNRAD_LIB=$PWD/variants/$v.so; fi
-  env $L timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"score_kernel|recheck_kernel" -c 3 --csv python tools/dyn_stats.py 2>/dev/null | grep -E "score_kernel|recheck_kernel" | awk -F'","' '{print substr($5,1,40), $NF}'
+  env $L timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"score_kernel|recheck_kernel|apply|job_stats" -c 5 --csv python tools/dyn_stats.py 2>/dev/null | grep -E "score_kernel|recheck_kernel|apply|job_stats" | awk -F'","' '{print substr($5,1,40), $NF}'
 done
