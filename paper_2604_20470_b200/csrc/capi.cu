@@ -935,16 +935,31 @@ static void layer_host(rp_plan plan, const rp_grid* g, const void* q_host, const
     const int hc = std::min(per, heads - h0);
     const size_t off = static_cast<size_t>(h0) * head_dim * es;
     const size_t w = static_cast<size_t>(hc) * head_dim * es;
-    for (auto pr : {std::make_pair(dq, q_host), std::make_pair(dk, k_host),
-                    std::make_pair(dv, v_host)})
-      RP_CUDA(cudaMemcpy2DAsync(pr.first + off, row_in, static_cast<const uint8_t*>(pr.second) + off,
-                                row_in, w, static_cast<size_t>(tokens), cudaMemcpyHostToDevice,
-                                hs.in));
+    auto h2d = [&](uint8_t* dst, const void* src, size_t o, size_t bytes) {
+      RP_CUDA(cudaMemcpy2DAsync(dst + o, row_in, static_cast<const uint8_t*>(src) + o, row_in,
+                                bytes, static_cast<size_t>(tokens), cudaMemcpyHostToDevice, hs.in));
+    };
+    // chunk 0: the scoring heads' Q/K go first, so stages (a)-(c) start
+    // while the rest of the chunk is still in flight
+    const int hs0 = c == 0 ? std::min(n_score_heads, hc) : 0;
+    const size_t ws = static_cast<size_t>(hs0) * head_dim * es;
+    if (hs0 > 0) {
+      h2d(dq, q_host, off, ws);
+      h2d(dk, k_host, off, ws);
+      cudaEvent_t score_in = event();
+      RP_CUDA(cudaEventRecord(score_in, hs.in));
+      RP_CUDA(cudaStreamWaitEvent(s, score_in, 0));
+    }
+    if (w > ws) {
+      h2d(dq, q_host, off + ws, w - ws);
+      h2d(dk, k_host, off + ws, w - ws);
+    }
+    h2d(dv, v_host, off, w);
     cudaEvent_t in_done = event();
     RP_CUDA(cudaEventRecord(in_done, hs.in));
-    RP_CUDA(cudaStreamWaitEvent(s, in_done, 0));
     if (c == 0) {
       // stages (a)-(c) from the first chunk (it holds the scoring heads)
+      if (hs0 == 0) RP_CUDA(cudaStreamWaitEvent(s, in_done, 0));
       rp_tensor tq{dq, dtype, tokens, hc, head_dim, ts, head_dim};
       rp_tensor tk = tq;
       tk.data = dk;
@@ -960,6 +975,7 @@ static void layer_host(rp_plan plan, const rp_grid* g, const void* q_host, const
       if (mask_out)
         RP_CUDA(cudaMemcpyAsync(mask_out, dm, mask_bytes, cudaMemcpyDeviceToHost, s));
     }
+    RP_CUDA(cudaStreamWaitEvent(s, in_done, 0));
     rp_tensor cq{dq + off, dtype, tokens, hc, head_dim, ts, head_dim};
     rp_tensor ck = cq, cv = cq, co = cq;
     ck.data = dk + off;
