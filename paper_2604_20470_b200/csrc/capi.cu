@@ -491,6 +491,32 @@ int e2e_chunks() {
   return n;
 }
 
+// Head-chunk sizes of the host-buffer pipelines: e2e_chunks() chunks of
+// ceil(heads / chunks) (at least min_first heads each), the last one split
+// into halves (5 -> 3, 1, 1): the exposed tail is the last piece's kernel
+// plus its D2H copy, so it is kept small (DYNRAD_E2E_TAPER=0: no split).
+std::vector<int> head_chunks(int heads, int min_first) {
+  static const bool taper = [] {
+    const char* e = std::getenv("DYNRAD_E2E_TAPER");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const int chunks = std::max(1, std::min(heads, e2e_chunks()));
+  const int per = std::max((heads + chunks - 1) / chunks, min_first);
+  std::vector<int> out;
+  for (int h0 = 0; h0 < heads; h0 += per) out.push_back(std::min(per, heads - h0));
+  if (taper && out.size() > 1) {
+    int last = out.back();
+    out.pop_back();
+    while (last > 1) {
+      const int a = (last + 1) / 2;
+      out.push_back(a);
+      last -= a;
+    }
+    if (last > 0) out.push_back(last);
+  }
+  return out;
+}
+
 }  // namespace rp
 
 using namespace rp;
@@ -795,8 +821,7 @@ static void host_attention(const rp_grid* g, const uint8_t* mask_bits_host, cons
     alloc(&dout, out_bytes);
     // Head-chunk pipeline over three streams: H2D of chunk c+1 and D2H of
     // chunk c-1 run under the kernel of chunk c (PCIe is full duplex).
-    const int chunks = std::max(1, std::min(heads, e2e_chunks()));
-    const int per = (heads + chunks - 1) / chunks;
+    const std::vector<int> sizes = head_chunks(heads, 1);
     HostStreams& hs = host_streams();
     cudaEvent_t start_ev;
     RP_CUDA(cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming));
@@ -809,9 +834,10 @@ static void host_attention(const rp_grid* g, const uint8_t* mask_bits_host, cons
       evs.push_back(e);
       return e;
     };
-    for (int h0 = 0; h0 < heads; h0 += per) {
-      const int hc = std::min(per, heads - h0);
+    int h0 = 0;
+    for (const int hc : sizes) {
       const size_t off = static_cast<size_t>(h0) * head_dim * es;
+      h0 += hc;
       const size_t w = static_cast<size_t>(hc) * head_dim * es;
       for (auto pr : {std::make_pair(dq, q_host), std::make_pair(dk, k_host),
                       std::make_pair(dv, v_host)})
@@ -907,8 +933,7 @@ static void layer_host(rp_plan plan, const rp_grid* g, const void* q_host, const
   alloc(&dv, in_bytes);
   alloc(&dout, out_bytes);
   RP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
-  const int chunks = std::max(1, std::min(heads, e2e_chunks()));
-  const int per = std::max((heads + chunks - 1) / chunks, n_score_heads);
+  const std::vector<int> sizes = head_chunks(heads, n_score_heads);
   HostStreams& hs = host_streams();
   std::vector<cudaEvent_t> evs;
   auto event = [&]() {
@@ -930,9 +955,8 @@ static void layer_host(rp_plan plan, const rp_grid* g, const void* q_host, const
   // Issue order per chunk: H2D(c), [c == 0: mask + row lists], attention(c),
   // D2H(c) -- interleaved so both copy directions stay busy (queueing every
   // H2D first measured 63 ms instead of 47 ms for the Wan layer).
-  int c = 0;
-  for (int h0 = 0; h0 < heads; h0 += per, ++c) {
-    const int hc = std::min(per, heads - h0);
+  int c = 0, h0 = 0;
+  for (const int hc : sizes) {
     const size_t off = static_cast<size_t>(h0) * head_dim * es;
     const size_t w = static_cast<size_t>(hc) * head_dim * es;
     auto h2d = [&](uint8_t* dst, const void* src, size_t o, size_t bytes) {
@@ -991,6 +1015,8 @@ static void layer_host(rp_plan plan, const rp_grid* g, const void* q_host, const
     RP_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(o_host) + off, row_in, dout + off, row_in, w,
                               static_cast<size_t>(g->padded_tokens), cudaMemcpyDeviceToHost,
                               hs.out));
+    h0 += hc;
+    ++c;
   }
   int hflag = 0;
   cudaEvent_t out_done = event();

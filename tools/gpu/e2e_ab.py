@@ -20,8 +20,11 @@ for name in ("layer", "exact_host"):
             gc = g.c()
             _lib.check(_lib.lib().rp_masked_attention_exact_host(C.byref(gc), C.c_void_p(mh.data_ptr()), C.c_void_p(qh.data_ptr()), C.c_void_p(kh.data_ptr()), C.c_void_p(vh.data_ptr()), 1, S, H, d, C.c_void_p(oh.data_ptr()), C.c_void_p(st.cuda_stream)))
     call()
-    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record(st)
-    for _ in range(5): call()
-    e1.record(st); st.synchronize()
-    print(name, e0.elapsed_time(e1) / 5)
+    ts = []
+    for rep in range(4):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(st)
+        for _ in range(5): call()
+        e1.record(st); st.synchronize()
+        ts.append(round(e0.elapsed_time(e1) / 5, 2))
+    print(os.environ.get("DYNRAD_E2E_TAPER", ""), name, ts, flush=True)
