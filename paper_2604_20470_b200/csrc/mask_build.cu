@@ -286,39 +286,114 @@ __global__ void exact_scores_kernel(const DJob* __restrict__ jobs,
 }
 
 // selection.cpp:133-142, sequential like the reference: bit-identical stats.
-__global__ void seq_stats_kernel(const int64_t* __restrict__ off, int n_jobs,
-                                 const float* __restrict__ scores, double2* __restrict__ stats) {
-  const int lj = blockIdx.x * blockDim.x + threadIdx.x;
+// The two fp64 chains (the sum, then the squared deviations from the mean)
+// stay in one thread in the reference's order; the block's other warps stage
+// the scores into shared memory chunk by chunk (double-buffered), so the
+// chain runs at the DADD latency instead of waiting on a global load per
+// score.  One block per frame pair.
+constexpr int kSeqChunk = 4096;
+constexpr int kSeqThreads = 256;
+__global__ void __launch_bounds__(kSeqThreads) seq_stats_kernel(const int64_t* __restrict__ off,
+                                                                int n_jobs,
+                                                                const float* __restrict__ scores,
+                                                                double2* __restrict__ stats,
+                                                                double* __restrict__ inv_den) {
+  __shared__ __align__(16) float buf[2][kSeqChunk];
+  const int lj = blockIdx.x;
   if (lj >= n_jobs) return;
   const float* s = scores + off[lj];
   const int64_t n = off[lj + 1] - off[lj];
-  double sum = 0.0;
-  for (int64_t x = 0; x < n; ++x) sum = __dadd_rn(sum, static_cast<double>(s[x]));
-  const double mean = __ddiv_rn(sum, static_cast<double>(n));
-  double sq = 0.0;
-  for (int64_t x = 0; x < n; ++x) {
-    const double dd = __dsub_rn(static_cast<double>(s[x]), mean);
-    sq = __dadd_rn(sq, __dmul_rn(dd, dd));
+  const int64_t nch = (n + kSeqChunk - 1) / kSeqChunk;
+  auto fill = [&](int b, int64_t c) {  // warps 1.. only: warp 0 runs the chain
+    if (threadIdx.x < 32) return;
+    const int64_t base = c * kSeqChunk;
+    const int cnt = static_cast<int>(n - base < kSeqChunk ? n - base : kSeqChunk);
+    for (int i = threadIdx.x - 32; i < cnt; i += kSeqThreads - 32) buf[b][i] = s[base + i];
+  };
+  double sum = 0.0, mean = 0.0, sq = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (nch > 0) fill(0, 0);
+    __syncthreads();
+    for (int64_t c = 0; c < nch; ++c) {
+      if (c + 1 < nch) fill(static_cast<int>((c + 1) & 1), c + 1);
+      if (threadIdx.x == 0) {
+        const float* b = buf[c & 1];
+        const int cnt = static_cast<int>(n - c * kSeqChunk < kSeqChunk ? n - c * kSeqChunk
+                                                                       : kSeqChunk);
+        int i = 0;
+        if (pass == 0) {
+#pragma unroll 4
+          for (; i + 4 <= cnt; i += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(b + i);
+            sum = __dadd_rn(sum, static_cast<double>(v.x));
+            sum = __dadd_rn(sum, static_cast<double>(v.y));
+            sum = __dadd_rn(sum, static_cast<double>(v.z));
+            sum = __dadd_rn(sum, static_cast<double>(v.w));
+          }
+          for (; i < cnt; ++i) sum = __dadd_rn(sum, static_cast<double>(b[i]));
+        } else {
+          auto step = [&](float x) {
+            const double dd = __dsub_rn(static_cast<double>(x), mean);
+            sq = __dadd_rn(sq, __dmul_rn(dd, dd));
+          };
+#pragma unroll 4
+          for (; i + 4 <= cnt; i += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(b + i);
+            step(v.x);
+            step(v.y);
+            step(v.z);
+            step(v.w);
+          }
+          for (; i < cnt; ++i) step(b[i]);
+        }
+      }
+      __syncthreads();
+    }
+    if (pass == 0) mean = __ddiv_rn(sum, static_cast<double>(n));
   }
-  stats[lj] = make_double2(mean, __dsqrt_rn(__ddiv_rn(sq, static_cast<double>(n))));
+  if (threadIdx.x == 0) {
+    const double sd = __dsqrt_rn(__ddiv_rn(sq, static_cast<double>(n)));
+    stats[lj] = make_double2(mean, sd);
+    if (inv_den) inv_den[lj] = 1.0 / __dadd_rn(sd, 1e-8);
+  }
 }
 
+// z >= tau per pair (selection.cpp:144-161).  z is the reference's
+// correctly rounded (s - mean) / (sd + 1e-8); a multiply by the frame pair's
+// reciprocal decides every pair whose z is not within 1e-13 (relative) of
+// tau, the rest take the exact division.  The frame pair's kept counter is
+// bumped once per warp and job.
 __global__ void exact_select_kernel(const DJob* __restrict__ jobs,
                                     const int* __restrict__ batch_jobs,
                                     const int64_t* __restrict__ off, int n_jobs, int64_t total,
                                     const float* __restrict__ scores,
-                                    const double2* __restrict__ stats, uint32_t* counts,
+                                    const double2* __restrict__ stats,
+                                    const double* __restrict__ inv_den, uint32_t* counts,
                                     unsigned long long* kept, int64_t nt, int bs) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= total) return;
-  const int lj = find_job(off, n_jobs, x);
-  const DJob& jb = jobs[batch_jobs[lj]];
-  if (zscore(scores[x], stats[lj]) >= jb.param) {
-    int64_t u, v;
-    band_uv(x - off[lj], nt, jb.width, &u, &v);
-    add_count(jb, counts, nt, bs, u, v);
-    atomicAdd(&kept[lj], 1ull);
+  const bool valid = x < total;
+  const int lj = valid ? find_job(off, n_jobs, x) : -1;
+  bool keep = false;
+  if (valid) {
+    const DJob& jb = jobs[batch_jobs[lj]];
+    const double2 st = stats[lj];
+    const double num = __dsub_rn(static_cast<double>(scores[x]), st.x);
+    const double tau = jb.param;
+    double z = __dmul_rn(num, inv_den[lj]);
+    if (fabs(z - tau) <= 1e-13 * (fabs(z) + fabs(tau)) || !isfinite(z))
+      z = __ddiv_rn(num, __dadd_rn(st.y, 1e-8));
+    keep = z >= tau;
+    if (keep) {
+      int64_t u, v;
+      band_uv(x - off[lj], nt, jb.width, &u, &v);
+      add_count(jb, counts, nt, bs, u, v);
+    }
   }
+  const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+  const unsigned same = __match_any_sync(0xFFFFFFFFu, lj);
+  const int lane = threadIdx.x & 31;
+  if (lj >= 0 && lane == __ffs(same) - 1 && (km & same))
+    atomicAdd(&kept[lj], static_cast<unsigned long long>(__popc(km & same)));
 }
 
 // selection.cpp:163-175: if nothing cleared tau keep the fallback_k best z,
@@ -711,6 +786,7 @@ void build_dynamic_exact(rp_plan_s& P, const Feat& f, uint32_t* words, int64_t* 
     d_off.upload(off.data(), nj + 1);
     DevBuf<float> scores(total, s);
     DevBuf<double2> stats(nj, s);
+    DevBuf<double> inv_den(nj, s);
     DevBuf<uint32_t> counts(ncnt, s);
     DevBuf<unsigned long long> kept(nj + 1, s);
     RP_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(uint32_t) * ncnt, s));
@@ -719,10 +795,10 @@ void build_dynamic_exact(rp_plan_s& P, const Feat& f, uint32_t* words, int64_t* 
     exact_scores_kernel<<<grid, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, nj, total, f, nt,
                                              scores.p);
     RP_LAUNCHED();
-    seq_stats_kernel<<<(nj + 63) / 64, 64, 0, s>>>(d_off.p, nj, scores.p, stats.p);
+    seq_stats_kernel<<<nj, kSeqThreads, 0, s>>>(d_off.p, nj, scores.p, stats.p, inv_den.p);
     RP_LAUNCHED();
     exact_select_kernel<<<grid, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, nj, total,
-                                             scores.p, stats.p, counts.p, kept.p, nt, bs);
+                                             scores.p, stats.p, inv_den.p, counts.p, kept.p, nt, bs);
     RP_LAUNCHED();
     exact_fallback_kernel<<<nj, 256, 0, s>>>(P.d_jobs.p, d_batch.p, d_off.p, scores.p, stats.p,
                                              kept.p, counts.p, nt, bs, P.c.fallback_k,
@@ -1020,7 +1096,7 @@ rp_status rp_normalize_scores(const float* scores_dev, int64_t n, double* z_dev,
     DevBuf<int64_t> d_off(2, s);
     d_off.upload(off, 2);
     DevBuf<double2> st(1, s);
-    seq_stats_kernel<<<1, 32, 0, s>>>(d_off.p, 1, scores_dev, st.p);
+    seq_stats_kernel<<<1, kSeqThreads, 0, s>>>(d_off.p, 1, scores_dev, st.p, nullptr);
     RP_LAUNCHED();
     zscore_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(scores_dev, n, st.p,
                                                                           z_dev);
