@@ -271,16 +271,33 @@ __global__ void token_to_block_kernel(const uint8_t* __restrict__ tok, int64_t d
 }
 
 // ------------------------------------ K2/K3 exact engine (fp64 SIMT) -------
+// One thread per band pair of the batch (flat index x).  The frame pair and
+// the band row are searched once per warp (lane 0) and each lane narrows
+// from there: a warp's 32 consecutive pairs span at most 32 band rows.
 __global__ void exact_scores_kernel(const DJob* __restrict__ jobs,
                                     const int* __restrict__ batch_jobs,
                                     const int64_t* __restrict__ off, int n_jobs, int64_t total,
                                     Feat f, int64_t nt, float* __restrict__ scores) {
-  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+  if (x0 >= total) return;
+  int lj0 = 0;
+  int64_t u0 = 0;
+  if (lane == 0) {
+    lj0 = find_job(off, n_jobs, x0);
+    int64_t v0;
+    band_uv(x0 - off[lj0], nt, jobs[batch_jobs[lj0]].width, &u0, &v0);
+  }
+  lj0 = __shfl_sync(0xFFFFFFFFu, lj0, 0);
+  u0 = __shfl_sync(0xFFFFFFFFu, u0, 0);
+  const int64_t x = x0 + lane;
   if (x >= total) return;
-  const int lj = find_job(off, n_jobs, x);
+  int lj = lj0;
+  while (x >= off[lj + 1]) ++lj;
   const DJob& jb = jobs[batch_jobs[lj]];
   int64_t u, v;
-  band_uv(x - off[lj], nt, jb.width, &u, &v);
+  if (lj == lj0) band_uv(x - off[lj], nt, jb.width, &u, &v, u0, u0 + 32);
+  else band_uv(x - off[lj], nt, jb.width, &u, &v);
   scores[x] = exact_score(f, static_cast<int64_t>(jb.i) * nt + u,
                           static_cast<int64_t>(jb.j) * nt + v);
 }
@@ -698,7 +715,9 @@ int64_t assign_counts(rp_plan_s& P, const std::vector<int>& batch) {
 }
 
 constexpr int64_t kDrawCap = int64_t{1} << 28;   // draws per static batch
-constexpr int64_t kScoreCap = int64_t{1} << 29;  // scores per exact batch
+// scores per exact batch (8 GB of fp32): every frame pair of a batch runs its
+// sequential stats chains concurrently, so fewer, larger batches cost less
+constexpr int64_t kScoreCap = int64_t{1} << 31;
 
 void build_static(rp_plan_s& P, uint32_t* words, cudaStream_t s) {
   const int bs = P.g.block_size;

@@ -25,9 +25,11 @@ RP_HD int64_t band_off(int64_t u, int64_t N, int64_t w) {
   if (c < 0) c = 0;
   return hi - c * (c + 1) / 2 + u;
 }
-// Flat index -> (u, v): largest u with off(u) <= flat (upper_bound - 1).
-RP_HD void band_uv(int64_t flat, int64_t N, int64_t w, int64_t* u, int64_t* v) {
-  int64_t lo = 0, hi = N;  // off(lo) <= flat < off(hi)
+// Flat index -> (u, v): largest u with off(u) <= flat (upper_bound - 1),
+// searched in [lo, hi) (off(lo) <= flat < off(hi); default the whole band).
+RP_HD void band_uv(int64_t flat, int64_t N, int64_t w, int64_t* u, int64_t* v, int64_t lo = 0,
+                   int64_t hi = -1) {
+  if (hi < 0 || hi > N) hi = N;
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
     if (band_off(mid, N, w) <= flat) lo = mid; else hi = mid;
@@ -89,6 +91,16 @@ RP_DEV float exact_score(const Feat& f, int64_t qrow, int64_t krow) {
           dot = __fma_rn(static_cast<double>(__uint_as_float(aw[t] & 0xFFFF0000u)),
                          static_cast<double>(__uint_as_float(bw[t] & 0xFFFF0000u)), dot);
         }
+      }
+    } else if (f.dtype == RP_F32 && ((qb | kb | f.d) & 3) == 0) {
+      const float4* qv = reinterpret_cast<const float4*>(static_cast<const float*>(f.q) + qb);
+      const float4* kv = reinterpret_cast<const float4*>(static_cast<const float*>(f.k) + kb);
+      for (int e = 0; e < f.d / 4; ++e) {
+        const float4 a = __ldg(qv + e), b = __ldg(kv + e);
+        dot = __fma_rn(static_cast<double>(a.x), static_cast<double>(b.x), dot);
+        dot = __fma_rn(static_cast<double>(a.y), static_cast<double>(b.y), dot);
+        dot = __fma_rn(static_cast<double>(a.z), static_cast<double>(b.z), dot);
+        dot = __fma_rn(static_cast<double>(a.w), static_cast<double>(b.w), dot);
       }
     } else {
       for (int e = 0; e < f.d; ++e)
