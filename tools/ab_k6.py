@@ -19,6 +19,13 @@ else:
                for _ in range(3))
 cfg = rp.SparsityConfig(rp.Mode.StaticRatio, rp.RadialParams(1.0, 0.1), 1.0, 0.2, 0.3, 0.3)
 mask = rp.Plan(g, cfg, 7).build_mask_device()
+if os.environ.get("DENSE"):  # every block active (per-flop efficiency without sparsity)
+    mask.fill_(255)
+    nb = g.blocks_per_dim
+    if nb % 8:
+        mask[:, nb // 8] = (1 << (nb % 8)) - 1
+    if mask.shape[1] > (nb + 7) // 8:
+        mask[:, (nb + 7) // 8:] = 0
 rpt, col, order = rp.mask_to_csr(g, mask)
 out = torch.empty((g.padded_tokens, H, d), dtype=torch.bfloat16, device="cuda")
 for _ in range(5):
