@@ -1005,6 +1005,10 @@ void fast_engine_run(FastEngine* e, const rp_tensor* q, const rp_tensor* k, cons
   p.ucap = static_cast<unsigned>(
       std::min<long long>(static_cast<long long>(e->items.size()) * kSlotsPerItem / grid,
                           0x7fffffffLL));
+  // DYNRAD_SCORE_UCAP: smaller per-CTA capacity (tests drive the in-place
+  // exact decision of pairs that overflow the list)
+  if (const char* cap = std::getenv("DYNRAD_SCORE_UCAP"))
+    p.ucap = std::min<unsigned>(p.ucap, static_cast<unsigned>(std::max(0, std::atoi(cap))));
   for (int mode = 0; mode < 2; ++mode) {
     const int st = mode == 0 ? kStageScoreStats : kStageScoreSelect;
     stage_begin(st, s);

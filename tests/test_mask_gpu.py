@@ -238,12 +238,14 @@ print("OK", int(fast.sum()))
 
 
 @pytest.mark.parametrize("env", [{"DYNRAD_SCORE_CG": "1"}, {"DYNRAD_SCORE_CG": "2"},
-                                 {"DYNRAD_SCORE_CG": "4"}, {"DYNRAD_SCORE_ORDER": "plain"}],
+                                 {"DYNRAD_SCORE_CG": "4"}, {"DYNRAD_SCORE_ORDER": "plain"},
+                                 {"DYNRAD_SCORE_UCAP": "1"}],
                          ids=lambda e: "-".join(f"{k}={v}" for k, v in e.items()))
 def test_fast_engine_schedules_are_exact(cuda, env):
     """Every epilogue width (warps per sub-partition) and work order of the
-    tensor-core scorer gives the exact engine's mask (read once per process,
-    so each runs in a subprocess)."""
+    tensor-core scorer, and the in-place exact decision of undecided pairs
+    that overflow a CTA's list (capacity forced to 1), give the exact
+    engine's mask (read once per process, so each runs in a subprocess)."""
     import os
     import subprocess
     import sys
