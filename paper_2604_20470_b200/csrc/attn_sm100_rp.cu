@@ -226,6 +226,107 @@ __global__ void pair_fill_kernel(const int32_t* __restrict__ row_ptr,
   }
 }
 
+// The same entry lists as pair_count_kernel / pair_fill_kernel, one WARP per
+// row pair: the two rows' blocks go into shared-memory bitmaps, common /
+// A-only / B-only blocks come out of the bitmap words in ascending order
+// (per-lane word ranges + a warp scan), so the lists are identical while a
+// pair no longer costs one thread's serial merge of both lists.  kWords
+// bounds S_b (32 * kWords blocks); larger grids use the per-thread kernels.
+constexpr int kPairWords = 64;     // S_b <= 2048
+constexpr int kPairWarps = 8;
+template <bool FILL>
+__global__ void __launch_bounds__(32 * kPairWarps)
+    pair_lists_warp_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                           int n_rows, int n_pairs, int32_t* __restrict__ counts,
+                           const int32_t* __restrict__ prow_ptr, int32_t* __restrict__ pcol,
+                           uint8_t* __restrict__ pflag) {
+  __shared__ uint32_t bm[kPairWarps][2][kPairWords];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * kPairWarps + w;
+  if (p >= n_pairs) return;
+  const int nw = (n_rows + 31) >> 5;
+  uint32_t* A = bm[w][0];
+  uint32_t* B = bm[w][1];
+  for (int x = lane; x < nw; x += 32) {
+    A[x] = 0u;
+    B[x] = 0u;
+  }
+  __syncwarp();
+  const int a = 2 * p, b = 2 * p + 1;
+  for (int i = row_ptr[a] + lane; i < row_ptr[a + 1]; i += 32) {
+    const int c = col[i];
+    atomicOr(&A[c >> 5], 1u << (c & 31));
+  }
+  if (b < n_rows)
+    for (int i = row_ptr[b] + lane; i < row_ptr[b + 1]; i += 32) {
+      const int c = col[i];
+      atomicOr(&B[c >> 5], 1u << (c & 31));
+    }
+  __syncwarp();
+  // lane l owns words [l * per, (l + 1) * per)
+  const int per = (nw + 31) >> 5;
+  const int w0 = lane * per, w1 = min(nw, w0 + per);
+  int mc = 0, ma = 0, mb = 0;
+  for (int x = w0; x < w1; ++x) {
+    mc += __popc(A[x] & B[x]);
+    ma += __popc(A[x] & ~B[x]);
+    mb += __popc(B[x] & ~A[x]);
+  }
+  int ic = mc, ia = ma, ib = mb;  // inclusive scans
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yc = __shfl_up_sync(0xFFFFFFFFu, ic, o);
+    const int ya = __shfl_up_sync(0xFFFFFFFFu, ia, o);
+    const int yb = __shfl_up_sync(0xFFFFFFFFu, ib, o);
+    if (lane >= o) {
+      ic += yc;
+      ia += ya;
+      ib += yb;
+    }
+  }
+  const int nc = __shfl_sync(0xFFFFFFFFu, ic, 31);
+  const int na = __shfl_sync(0xFFFFFFFFu, ia, 31);
+  const int nb = __shfl_sync(0xFFFFFFFFu, ib, 31);
+  if (!FILL) {
+    if (lane == 0) counts[p] = nc + (na > nb ? na : nb);
+    return;
+  }
+  const int o = prow_ptr[p];
+  const int m = na < nb ? na : nb;
+  int kc = ic - mc, ka = ia - ma, kb = ib - mb;
+  for (int x = w0; x < w1; ++x) {
+    for (uint32_t v = A[x] & B[x]; v; v &= v - 1) {
+      const int c = 32 * x + __ffs(v) - 1;
+      pcol[2 * (o + kc)] = c;
+      pcol[2 * (o + kc) + 1] = c;
+      pflag[o + kc] = 3;
+      ++kc;
+    }
+    for (uint32_t v = A[x] & ~B[x]; v; v &= v - 1) {
+      const int c = 32 * x + __ffs(v) - 1;
+      const int e = o + nc + ka;  // split (ka < m) or leftover (then na > nb)
+      pcol[2 * e] = c;
+      if (ka < m) {
+        pflag[e] = 1 | 2 | 4;
+      } else {
+        pcol[2 * e + 1] = -1;
+        pflag[e] = 1;
+      }
+      ++ka;
+    }
+    for (uint32_t v = B[x] & ~A[x]; v; v &= v - 1) {
+      const int c = 32 * x + __ffs(v) - 1;
+      const int e = o + nc + kb;
+      pcol[2 * e + 1] = c;
+      if (kb >= m) {
+        pcol[2 * e] = -1;
+        pflag[e] = 2;
+      }
+      ++kb;
+    }
+  }
+}
+
 template <int D, bool SOFT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     bsfa_fwd_rp_kernel(const __grid_constant__ CUtensorMap tq,

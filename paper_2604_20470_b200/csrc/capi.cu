@@ -276,14 +276,27 @@ static void launch_attention(const rp_grid& g, const rp_tensor& q, const rp_tens
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prow), sizeof(int32_t) * (n_pairs + 1), stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pcol), sizeof(int32_t) * 2 * cap, stream));
       RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pflag), cap, stream));
-      const unsigned pg = static_cast<unsigned>((n_pairs + 127) / 128);
-      attn3::pair_count_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, pcnt);
-      RP_LAUNCHED();
-      csr::scan_kernel<<<1, 1024, 0, stream>>>(pcnt, n_pairs, prow, nullptr);
-      RP_LAUNCHED();
-      attn3::pair_fill_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, prow,
-                                                     pcol, pflag);
-      RP_LAUNCHED();
+      if (n_rows <= 32 * attn3::kPairWords && !std::getenv("DYNRAD_RP_SERIAL_LISTS")) {
+        const unsigned wg = static_cast<unsigned>((n_pairs + attn3::kPairWarps - 1) /
+                                                  attn3::kPairWarps);
+        attn3::pair_lists_warp_kernel<false><<<wg, 32 * attn3::kPairWarps, 0, stream>>>(
+            row_ptr, col_idx, n_rows, n_pairs, pcnt, nullptr, nullptr, nullptr);
+        RP_LAUNCHED();
+        csr::scan_kernel<<<1, 1024, 0, stream>>>(pcnt, n_pairs, prow, nullptr);
+        RP_LAUNCHED();
+        attn3::pair_lists_warp_kernel<true><<<wg, 32 * attn3::kPairWarps, 0, stream>>>(
+            row_ptr, col_idx, n_rows, n_pairs, nullptr, prow, pcol, pflag);
+        RP_LAUNCHED();
+      } else {
+        const unsigned pg = static_cast<unsigned>((n_pairs + 127) / 128);
+        attn3::pair_count_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, pcnt);
+        RP_LAUNCHED();
+        csr::scan_kernel<<<1, 1024, 0, stream>>>(pcnt, n_pairs, prow, nullptr);
+        RP_LAUNCHED();
+        attn3::pair_fill_kernel<<<pg, 128, 0, stream>>>(row_ptr, col_idx, n_rows, n_pairs, prow,
+                                                       pcol, pflag);
+        RP_LAUNCHED();
+      }
       attn3::Params p;
       p.row_ptr = row_ptr;
       p.prow_ptr = prow;
