@@ -920,17 +920,18 @@ static void launch_pass_cg(const CUtensorMap& mq, const CUtensorMap& mk, const S
 }
 
 // Epilogue column groups (warps per sub-partition, see Epi) per pass.
-// Measured at the Hunyuan shape (profiles/r1_score_ablation.md): the stats
-// pass is feed-bound and runs best with CG = 1; the select pass's longer
-// epilogue gains ~9 % from two warps per sub-partition.  DYNRAD_SCORE_CG in
-// {1, 2, 4} forces both.
+// Measured at the Hunyuan shape (ncu, profiles/r2_score_notes.md): two warps
+// per sub-partition for both passes (stats 5.38 -> 4.99 ms once its
+// reduction moved to one per unit; select 8.26 ms at CG = 1, 6.82 at 2,
+// 7.61 at 4).  DYNRAD_SCORE_CG in {1, 2, 4} forces both.
 static int score_cg(int mode) {
   static const int forced = [] {
     const char* e = std::getenv("DYNRAD_SCORE_CG");
     const int v = e ? std::atoi(e) : 0;
     return (v == 1 || v == 2 || v == 4) ? v : 0;
   }();
-  return forced ? forced : (mode == 0 ? 1 : 2);
+  (void)mode;
+  return forced ? forced : 2;
 }
 
 template <int NC>
