@@ -511,6 +511,28 @@ def measure(args, ctx, cfgd, peaks, steps, full=True):
                     "per_launch": f"2*d*H_f*P_band = {alg / 1e12:.2f} TFLOP "
                                   f"({sp} scored token pairs on this rank)"}
         rec["build_stats"] = build_stats
+        # stages (a) K5 and (c) on HBM: latency-bound at these
+        # sizes, so the microseconds are the figure; the fraction is the
+        # algorithmic bytes over the measured HBM bandwidth
+        hbm = peaks["hbm_gbs"]
+        nbk = g.blocks_per_dim
+        mask_bytes = nbk * g.row_bytes
+        stage_bytes = {
+            # bitmask read; row_ptr, col_idx, row order written
+            "csr": mask_bytes + 4 * (nbk + 1) + 4 * nnz + 4 * nbk,
+            # per-tile column counts read, mask written, mu / sigma per frame pair
+            "apply": mask_bytes + 16 * build_stats.get("retained_frame_pairs", 0),
+            # Q'/K' of the scoring heads read once, per-token norms written
+            "mask_prep": 2 * S * N_SCORE_HEADS * d * 2 + 2 * g.padded_tokens * 4,
+        }
+        rec["hbm_stage_rooflines"] = {}
+        for name, b in stage_bytes.items():
+            t = stage_ms.get(name)
+            if t:
+                rec["hbm_stage_rooflines"][name] = {
+                    "bound": "hbm", "us": t * 1e3, "algorithmic_bytes": int(b),
+                    "achieved": b / (t * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": b / (t * 1e-3) / 1e9 / hbm}
 
     # ---- optional all-gather of the head-sharded outputs ----------------------
     if args.gather and world > 1:
@@ -789,7 +811,9 @@ def main():
         for key in ("config", "effective_tflops", "algorithmic_tflops", "mask_build_ms_one_time",
                     "static_mask_build_ms_warm", "roofline", "roofline_sustained_frac", "clocks",
                     "gpu_launches", "e2e", "gather_ms", "value_with_gather", "dense",
-                    "library_comparator", "stages_ms", "per_step_ms"):
+                    "library_comparator", "stages_ms", "per_step_ms", "scoring_roofline",
+                    "hbm_stage_rooflines", "build_stats", "mask_equals_reference_golden",
+                    "pooled_selector_f1"):
             if key in rec:
                 line[key] = rec[key]
         line["roofline"]["peak_source"] = f"{peaks_kind} bf16_tflops (burst)"
