@@ -13,16 +13,18 @@
 // K = H_f * d.  Bf16 products are exact, so a fast score differs from the
 // reference's double-accumulated score only by the fp32 accumulation inside
 // the tensor core, bounded per pair by kappa * |q'_u| |k'_v| (Cauchy-Schwarz).
-//   pass 1 (stats): per item and row, two-pass (n, mean, M2) in registers,
-//          Chan-merged in double across rows; items are then merged per
-//          frame pair in a fixed order (deterministic mu / sigma).
+//   pass 1 (stats): per row fp32 sums of a tile, carried in fp64 across the
+//          unit (one frame pair, one tile row), reduced once per unit to
+//          (n, mean, M2); units are then Chan-merged per frame pair in a
+//          fixed order (deterministic mu / sigma).
 //   pass 2 (select): z = (s - mu)/(sigma + 1e-8); decided directly when
 //          |z - tau| exceeds the pair's error bound + delta_floor, otherwise
-//          queued; kept bits -> per-column counts by warp ballots -> the
-//          frame pair's [tile][B] count buffer.
+//          appended to the CTA's undecided region; kept bits -> per-column
+//          counts by 32 x 32 bit transposes -> the frame pair's [tile][B]
+//          count buffer.
 //   recheck: every queued pair is re-scored exactly as the reference does
 //          (fp64, sequential d, separate multiply / add, float cast).
-//   apply: theta_c / theta_m per tile (shared with the exact engine).
+//   apply: theta_c / theta_m per tile, one warp per tile.
 // Frame pairs with no kept pair take the fallback_k rule on exact scores
 // (it can only change a tile when fallback_k >= ceil(theta_c * B)).
 #include <algorithm>
@@ -641,8 +643,8 @@ __global__ void tile_max_kernel(const float* __restrict__ norms, long long token
 }
 
 // Exact re-score of every undecided pair (reference operation order): one
-// thread per (item, warp) slot group.
-// blockIdx.y = the scoring CTA whose undecided region this block walks.
+// thread per pair; blockIdx.y = the scoring CTA whose undecided region this
+// block walks.
 __global__ void recheck_kernel(const DJob* __restrict__ jobs, const uint2* __restrict__ upairs,
                                const unsigned* __restrict__ ucount, unsigned ucap, Feat f,
                                const double2* __restrict__ job_stats, uint32_t* counts,
