@@ -15,3 +15,8 @@ for it in range(3):
 rp.profile_stages(True)
 p = rp.Plan(g, cfg, 5); d = p.build_mask_device(); torch.cuda.synchronize()
 print(rp.profile_read())
+# host vs device split of one plan build
+t0 = time.perf_counter(); p = rp.Plan(g, cfg, 5); t1 = time.perf_counter()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record(); d = p.build_mask_device(); e1.record(); t2 = time.perf_counter(); torch.cuda.synchronize(); t3 = time.perf_counter()
+print(f"plan create {1e3*(t1-t0):.1f} ms, build call returns after {1e3*(t2-t1):.1f} ms, device {e0.elapsed_time(e1):.1f} ms, total {1e3*(t3-t0):.1f} ms")
