@@ -395,8 +395,8 @@ rp_status rp_block_mean_pool(const rp_grid* g, const rp_tensor* x, int n_heads, 
     const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(x->data);
     pooled::pool_kernel<<<dim3(static_cast<unsigned>(g->blocks_per_dim), 1), 256, 0,
                           reinterpret_cast<cudaStream_t>(stream)>>>(
-        p, p, x->token_stride, x->head_stride, n_heads, x->head_dim, g->total_tokens,
-        g->block_size, out_dev, out_dev);
+        p, nullptr, x->token_stride, x->head_stride, n_heads, x->head_dim, g->total_tokens,
+        g->block_size, out_dev, nullptr);  // gridDim.y = 1: only the Q side
     RP_LAUNCHED();
   });
 }
