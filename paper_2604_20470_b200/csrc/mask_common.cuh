@@ -27,9 +27,33 @@ RP_HD int64_t band_off(int64_t u, int64_t N, int64_t w) {
 }
 // Flat index -> (u, v): largest u with off(u) <= flat (upper_bound - 1),
 // searched in [lo, hi) (off(lo) <= flat < off(hi); default the whole band).
+// The same offsets in 32-bit arithmetic: exact while N^2 < 2^31 (N <= 46340;
+// w is clamped to N, which leaves off(u) unchanged).
+RP_HD int32_t band_off32(int32_t u, int32_t N, int32_t w) {
+  int32_t a = N - w;
+  if (a < 0) a = 0;
+  if (a > u) a = u;
+  const int32_t hi = a * (a - 1) / 2 + a * w + (u - a) * (N - 1);
+  int32_t c = u - 1 - w;
+  if (c < 0) c = 0;
+  return hi - c * (c + 1) / 2 + u;
+}
 RP_HD void band_uv(int64_t flat, int64_t N, int64_t w, int64_t* u, int64_t* v, int64_t lo = 0,
                    int64_t hi = -1) {
   if (hi < 0 || hi > N) hi = N;
+  if (N <= 46340) {  // frame sizes in practice: the search in 32-bit arithmetic
+    const int32_t n32 = static_cast<int32_t>(N);
+    const int32_t w32 = static_cast<int32_t>(w < N ? w : N);
+    const int32_t f32 = static_cast<int32_t>(flat);
+    int32_t l32 = static_cast<int32_t>(lo), h32 = static_cast<int32_t>(hi);
+    while (h32 - l32 > 1) {
+      const int32_t mid = (l32 + h32) >> 1;
+      if (band_off32(mid, n32, w32) <= f32) l32 = mid; else h32 = mid;
+    }
+    *u = l32;
+    *v = (l32 - w32 > 0 ? l32 - w32 : 0) + (f32 - band_off32(l32, n32, w32));
+    return;
+  }
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
     if (band_off(mid, N, w) <= flat) lo = mid; else hi = mid;
