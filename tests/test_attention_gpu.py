@@ -151,6 +151,37 @@ def test_wan_shape_bf16_vs_oracle_sampled_rows(cuda, port):
     assert worst < 2e-2, worst
 
 
+def test_hunyuan_shape_default_kernel_vs_oracle_sampled_rows(cuda, port):
+    """Production shape above the auto rule's threshold (HunyuanVideo 61x3600,
+    B = 128, one head's K + V = 112 MB > 64 MiB, so the default environment
+    runs the row-pair kernel) on the reference's own config-4 dynamic mask
+    (tests/golden/hunyuan_mid.drbm, 0.8074 sparsity): sampled query rows
+    against the C restatement of attention.cpp:50-106."""
+    import os
+    if os.environ.get("DYNRAD_K6"):
+        pytest.skip("checks the default kernel choice")
+    from golden_util import GOLDEN, read_drbm
+    g = rp.make_grid(61, 3600, 128)
+    dim, bits = read_drbm(f"{GOLDEN}/hunyuan_mid.drbm")
+    assert dim == g.blocks_per_dim
+    mask = torch.from_numpy(np.ascontiguousarray(bits)).cuda()
+    row_ptr, col_idx, order = rp.mask_to_csr(g, mask)
+    assert int(col_idx.numel()) == 567038
+    H, d, S = 2, 128, g.total_tokens
+    assert rp.attention_kernel(g, "bf16", d).startswith("bsfa_fwd_rp_kernel")
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    q, k, v = (torch.randn((S, H, d), device="cuda", generator=gen).to(torch.bfloat16)
+               for _ in range(3))
+    out = rp.sparse_attention(g, q, k, v, row_ptr, col_idx, order).float().cpu().numpy()
+    qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))
+    worst = 0.0
+    for r0 in (0, 3596, 100000, 219600 - 8, 219640):  # incl. a frame edge and the padded tail
+        r1 = min(r0 + 8, g.padded_tokens)
+        ref = port.masked_attention_exact(61, 3600, 128, bits, qn, kn, vn, r0, r1, threads=8)
+        worst = max(worst, rel_rows(out[r0:r1], ref))
+    assert worst < 2e-2, worst
+
+
 def test_empty_row_gives_zeros_on_device(cuda):
     """The device entry point cannot raise mid-stream: a block row with no
     active block is written as zeros (the host/facade entry points raise the
