@@ -33,3 +33,20 @@ for hp in (1, 2, 5, 10, 20, 40):
 def d2h():
     with torch.cuda.stream(st): x.copy_(y, non_blocking=True)
 t = timed(d2h); print(f"D2H contiguous {t:.2f} ms {nbytes/t/1e6:.1f} GB/s")
+# two H2D streams in parallel (halves of the tensor)
+st2 = torch.cuda.Stream()
+half = S // 2
+def two():
+    with torch.cuda.stream(st):
+        y[:half].copy_(x[:half], non_blocking=True)
+    with torch.cuda.stream(st2):
+        y[half:].copy_(x[half:], non_blocking=True)
+def timed2(fn, reps=5):
+    fn(); torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    for _ in range(reps): fn()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) * 1e3 / reps
+t = timed2(two); print(f"H2D two streams {t:.2f} ms {nbytes/t/1e6:.1f} GB/s")
+t = timed2(contig); print(f"H2D one stream (wall) {t:.2f} ms {nbytes/t/1e6:.1f} GB/s")
